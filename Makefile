@@ -1,0 +1,32 @@
+# libnorm build: CUDA for sm_100a only, plus the CPU oracle and the input generator.
+NVCC    ?= /usr/local/cuda/bin/nvcc
+CC      ?= gcc
+PYSITE  := $(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])" 2>/dev/null)
+NCCL_DIR ?= $(PYSITE)/nvidia/nccl
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Xptxas -v --expt-relaxed-constexpr -Iinclude -I$(NCCL_DIR)/include
+PKG     := paper_2207_00257_b200
+CSRC    := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cpp)
+CHDR    := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/libnorm.h
+
+all: oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
+
+# Oracle: plain C, no contraction, no fast-math, no threads; shares nothing with the CUDA path.
+oracle/liboracle.so: oracle/norm_oracle.c oracle/norm_oracle.h
+	$(CC) -std=c11 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
+
+gen/libnormgen.so: gen/gen_host.c gen/norm_gen.h
+	$(CC) -std=c11 -O2 -pthread -fPIC -shared -o $@ $< -lpthread
+
+gen/libnormgen_cuda.so: gen/gen_cuda.cu gen/norm_gen.h
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
+
+$(PKG)/libnorm.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+
+clean:
+	rm -f oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
+
+.PHONY: all clean

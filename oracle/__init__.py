@@ -1,0 +1,151 @@
+"""CPU oracle for Fig. 1 `normalize` — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  It wraps the plain C oracle
+``oracle/norm_oracle.c`` (fp64 + exact superaccumulator) with ctypes over numpy
+arrays; it shares no code with the CUDA path.  See ``norm_oracle.h`` for the
+passage each function follows and its parity-pin status.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+LITERAL, DENSE = 0, 1
+_MODES = {"literal": LITERAL, "dense": DENSE}
+_lib = None
+
+
+def _mode(m):
+    return _MODES[m] if isinstance(m, str) else int(m)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(_DIR, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(path)
+        i64, vp, u64p = ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)
+        L.oracle_grid_blocks.argtypes = [i64]
+        L.oracle_grid_blocks.restype = i64
+        L.oracle_tid.argtypes = [i64, i64, ctypes.c_int]
+        L.oracle_tid.restype = i64
+        L.oracle_coverage_brute.argtypes = [i64, ctypes.c_int, vp]
+        L.oracle_coverage_closed.argtypes = [i64, ctypes.c_int, ctypes.POINTER(i64),
+                                             ctypes.POINTER(i64)]
+        L.oracle_is_covered.argtypes = [i64, ctypes.c_int, i64]
+        for f in ("oracle_sum_seq", "oracle_sum_exact", "oracle_sum_abs_exact"):
+            getattr(L, f).argtypes = [vp, i64]
+            getattr(L, f).restype = ctypes.c_double
+        for f in ("oracle_form_thread", "oracle_form_block", "oracle_form_hoisted"):
+            getattr(L, f).argtypes = [vp, vp, i64, ctypes.c_int, u64p]
+        L.oracle_rows.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
+        L.oracle_replay.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float]
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.ctypes.data
+
+
+def grid_blocks(n):
+    return lib().oracle_grid_blocks(n)
+
+
+def tid(b, t, mode="literal"):
+    return lib().oracle_tid(b, t, _mode(mode))
+
+
+def coverage_brute(n, mode="literal"):
+    mult = np.zeros(max(n, 1), dtype=np.uint32)
+    assert lib().oracle_coverage_brute(n, _mode(mode), mult.ctypes.data) == 0
+    return mult[:n]
+
+
+def coverage_closed(n, mode="literal"):
+    c, p = ctypes.c_int64(), ctypes.c_int64()
+    assert lib().oracle_coverage_closed(n, _mode(mode), ctypes.byref(c), ctypes.byref(p)) == 0
+    return c.value, p.value
+
+
+def is_covered(n, i, mode="literal"):
+    return bool(lib().oracle_is_covered(n, _mode(mode), i))
+
+
+def covered_mask(n, mode="literal"):
+    """Boolean mask of C(n) from the closed form (vectorised over i)."""
+    count, prefix = coverage_closed(n, mode)
+    i = np.arange(n, dtype=np.int64)
+    if prefix >= 0:
+        return i < prefix
+    G = grid_blocks(n)
+    return (i % 32) < G
+
+
+def sum_seq(x):
+    x, p = _f32(x)
+    return lib().oracle_sum_seq(p, x.size)
+
+
+def sum_exact(x):
+    x, p = _f32(x)
+    return lib().oracle_sum_exact(p, x.size)
+
+
+def sum_abs_exact(x):
+    x, p = _f32(x)
+    return lib().oracle_sum_abs_exact(p, x.size)
+
+
+def _form(fname, inp, mode, out=None):
+    inp, pin = _f32(inp)
+    if out is None:
+        out = np.zeros_like(inp)
+    assert out.dtype == np.float32 and out.flags["C_CONTIGUOUS"] and out.size == inp.size
+    adds = ctypes.c_uint64(0)
+    rc = getattr(lib(), fname)(out.ctypes.data, pin, inp.size, _mode(mode), ctypes.byref(adds))
+    if rc:
+        raise ValueError(f"{fname} rejected its arguments")
+    return out, adds.value
+
+
+def form_thread(inp, mode="literal", out=None):
+    """Fig. 1 as written: O(N^2) adds. Returns (out, adds)."""
+    return _form("oracle_form_thread", inp, mode, out)
+
+
+def form_block(inp, mode="literal", out=None):
+    """Per-block shared-memory variant: O(N^2/B) adds."""
+    return _form("oracle_form_block", inp, mode, out)
+
+
+def form_hoisted(inp, mode="literal", out=None):
+    """After parallel LICM: O(N) adds."""
+    return _form("oracle_form_hoisted", inp, mode, out)
+
+
+def normalize(inp, mode="literal", out=None):
+    return form_hoisted(inp, mode, out)[0]
+
+
+def rows(inp2d, mode="literal", out=None):
+    inp2d = np.ascontiguousarray(inp2d, dtype=np.float32)
+    R, C = inp2d.shape
+    if out is None:
+        out = np.zeros_like(inp2d)
+    rc = lib().oracle_rows(out.ctypes.data, inp2d.ctypes.data, R, C, out.shape[1], C, _mode(mode))
+    assert rc == 0
+    return out
+
+
+def replay(inp, s, mode="literal", out=None):
+    inp, pin = _f32(inp)
+    if out is None:
+        out = np.zeros_like(inp)
+    assert lib().oracle_replay(out.ctypes.data, pin, inp.size, _mode(mode), float(s)) == 0
+    return out

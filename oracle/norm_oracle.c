@@ -1,0 +1,250 @@
+/*
+ * oracle/norm_oracle.c — CPU oracle for Fig. 1 `normalize` (arxiv 2207.00257).
+ *
+ * TEST INFRASTRUCTURE ONLY (see norm_oracle.h).  Compiled with
+ * -O2 -ffp-contract=off -fno-fast-math; no SIMD intrinsics, no threads.
+ *
+ * What the oracle computes (Fig. 1, and §2.1):
+ *   for every (blockIdx b, threadIdx t) of normalize<<<(n+31)/32, 32>>>:
+ *       tid = b + 32 t                (literal index)
+ *       val = sum(in, n)              (`sum` elided at :100)
+ *       if (tid < n) out[tid] = in[tid] / val
+ * Form 1 evaluates `sum` per thread (as written), form 2 once per block (the
+ * commented shared-memory variant), form 3 once before the
+ * grid (after parallel LICM).
+ */
+#include "norm_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define FIG1_BLOCK 32 /* blockDim.x of the launch */
+
+/* ------------------------------------------------------------------ launch */
+
+int64_t oracle_grid_blocks(int64_t n) { return (n + 31) / 32; /* PAPER.md:113 */ }
+
+int64_t oracle_tid(int64_t b, int64_t t, int mode) {
+  if (mode == ORACLE_LITERAL) return b + (int64_t)FIG1_BLOCK * t;
+  return b * (int64_t)FIG1_BLOCK + t;                             /* reading R1   */
+}
+
+/* ---------------------------------------------------------------- coverage */
+
+int oracle_coverage_brute(int64_t n, int mode, uint32_t* mult) {
+  if (n < 0 || (n > 0 && !mult)) return 1;
+  if (n > 0) memset(mult, 0, (size_t)n * sizeof(uint32_t));
+  int64_t G = oracle_grid_blocks(n);
+  for (int64_t b = 0; b < G; ++b)
+    for (int64_t t = 0; t < FIG1_BLOCK; ++t) {
+      int64_t tid = oracle_tid(b, t, mode);
+      if (tid < n) mult[tid] += 1; /* `if (tid < n)` */
+    }
+  return 0;
+}
+
+/* Closed form: tid = b + 32t with 0 <= b < G, 0 <= t < 32.
+ *  G >= 32: the b-range spans every residue mod 32, so tids fill [0, G-1+992]
+ *           without gaps; C(n) = [0, min(n, G+992)).
+ *  G <  32: tid mod 32 = b, so C(n) = {x < n : x mod 32 < G}.            */
+int oracle_is_covered(int64_t n, int mode, int64_t i) {
+  if (i < 0 || i >= n) return 0;
+  if (mode != ORACLE_LITERAL) return 1;
+  int64_t G = oracle_grid_blocks(n);
+  if (G >= 32) return i < G + 992;
+  return (i % 32) < G;
+}
+
+int oracle_coverage_closed(int64_t n, int mode, int64_t* count, int64_t* prefix_len) {
+  if (n < 0 || !count || !prefix_len) return 1;
+  if (n == 0) { *count = 0; *prefix_len = 0; return 0; }
+  if (mode != ORACLE_LITERAL) { *count = n; *prefix_len = n; return 0; }
+  int64_t G = oracle_grid_blocks(n);
+  if (G >= 32) {
+    int64_t L = n < G + 992 ? n : G + 992;
+    *count = L;
+    *prefix_len = L;
+    return 0;
+  }
+  int64_t rem = n % 32;
+  *count = (n / 32) * G + (rem < G ? rem : G);
+  *prefix_len = (n <= 32) ? 1 : -1; /* C = {0} when G == 1 */
+  return 0;
+}
+
+/* -------------------------------------------------------------------- sums */
+
+/* Reading R2: sum(data, n) = sum_{i<n} data[i], PAPER.md:100 (body elided). */
+double oracle_sum_seq(const float* x, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += (double)x[i];
+  return s;
+}
+
+/* Exact superaccumulator.  A finite binary32 value is mant * 2^(k - 149) with
+ * integer mant < 2^24 and k in [0, 253]; the accumulator holds the integer
+ * sum_i (+-mant_i << k_i) in 32-bit digits stored in int64 limbs (headroom for
+ * 2^30 additions between carry normalisations). */
+#define ACC_LIMBS 12
+typedef struct {
+  int64_t limb[ACC_LIMBS];
+  int64_t pending;
+  int64_t nposinf, nneginf, nnan, nterms, nnegzero;
+} acc_t;
+
+static void acc_norm(acc_t* a) {
+  for (int j = 0; j < ACC_LIMBS - 1; ++j) {
+    int64_t low = a->limb[j] & 0xFFFFFFFFll;
+    int64_t carry = (a->limb[j] - low) / 4294967296ll; /* exact: divisible */
+    a->limb[j] = low;
+    a->limb[j + 1] += carry;
+  }
+  a->pending = 0;
+}
+
+static void acc_add(acc_t* a, float f, int absolute) {
+  uint32_t u;
+  memcpy(&u, &f, sizeof u);
+  uint32_t sign = u >> 31, e = (u >> 23) & 0xFFu, m = u & 0x7FFFFFu;
+  if (absolute) sign = 0;
+  a->nterms++;
+  if (e == 0xFFu) {
+    if (m) a->nnan++;
+    else if (sign) a->nneginf++;
+    else a->nposinf++;
+    return;
+  }
+  if (e == 0 && m == 0 && sign) a->nnegzero++;
+  uint64_t mant = e ? (m | 0x800000u) : m;
+  int k = e ? (int)e - 1 : 0;
+  uint64_t v = mant << (k % 32);
+  int j = k / 32;
+  int64_t lo = (int64_t)(v & 0xFFFFFFFFull), hi = (int64_t)(v >> 32);
+  if (sign) { a->limb[j] -= lo; a->limb[j + 1] -= hi; }
+  else      { a->limb[j] += lo; a->limb[j + 1] += hi; }
+  if (++a->pending == (1ll << 30)) acc_norm(a);
+}
+
+static int acc_bit(const int64_t* d, int p) { return (int)((d[p / 32] >> (p % 32)) & 1); }
+
+/* Round the exact integer (times 2^-149) to the nearest double, ties to even. */
+static double acc_result(acc_t* a) {
+  if (a->nnan || (a->nposinf && a->nneginf)) return NAN; /* reading R7 */
+  if (a->nposinf) return INFINITY;
+  if (a->nneginf) return -INFINITY;
+  acc_norm(a);
+  int neg = a->limb[ACC_LIMBS - 1] < 0;
+  if (neg) {
+    for (int j = 0; j < ACC_LIMBS; ++j) a->limb[j] = -a->limb[j];
+    acc_norm(a);
+  }
+  int top = -1;
+  for (int p = 32 * ACC_LIMBS - 1; p >= 0; --p)
+    if (acc_bit(a->limb, p)) { top = p; break; }
+  if (top < 0) /* exact zero: -0 only if every term was -0 (IEEE sum) */
+    return (a->nterms > 0 && a->nnegzero == a->nterms) ? -0.0 : 0.0;
+  uint64_t M = 0;
+  int low = top - 52 > 0 ? top - 52 : 0;
+  for (int p = top; p >= low; --p) M = (M << 1) | (uint64_t)acc_bit(a->limb, p);
+  if (low > 0) {
+    int round = acc_bit(a->limb, low - 1), sticky = 0;
+    for (int p = low - 2; p >= 0 && !sticky; --p) sticky = acc_bit(a->limb, p);
+    if (round && (sticky || (M & 1))) M += 1; /* 2^53 is still exact */
+  }
+  double r = ldexp((double)M, low - 149);
+  return neg ? -r : r;
+}
+
+static double exact_sum(const float* x, int64_t n, int absolute) {
+  acc_t a;
+  memset(&a, 0, sizeof a);
+  for (int64_t i = 0; i < n; ++i) acc_add(&a, x[i], absolute);
+  return acc_result(&a);
+}
+
+double oracle_sum_exact(const float* x, int64_t n) { return exact_sum(x, n, 0); }
+double oracle_sum_abs_exact(const float* x, int64_t n) { return exact_sum(x, n, 1); }
+
+/* The oracle's `sum`: the exact S rounded once to fp64 (reading R2/R3). */
+static double fig1_sum(const float* data, int64_t n, uint64_t* adds) {
+  if (adds) *adds += (uint64_t)n; /* one add per element: O(n) per call */
+  return oracle_sum_exact(data, n);
+}
+
+/* out[tid] = in[tid] / val, quotient rounded once to fp32. */
+static float fig1_div(float a, double val) { return (float)((double)a / val); }
+
+/* ------------------------------------------------------------------- forms */
+
+/* Form 1, as written: `float val = sum(in, n);` in every thread. */
+int oracle_form_thread(float* out, const float* in, int64_t n, int mode, uint64_t* adds) {
+  if (n < 0 || (n > 0 && (!out || !in)) || (n > 0 && out == in)) return 1;
+  int64_t G = oracle_grid_blocks(n);
+  for (int64_t b = 0; b < G; ++b)
+    for (int64_t t = 0; t < FIG1_BLOCK; ++t) {
+      double val = fig1_sum(in, n, adds);
+      int64_t tid = oracle_tid(b, t, mode);
+      if (tid < n) out[tid] = fig1_div(in[tid], val);
+    }
+  return 0;
+}
+
+/* Form 2, the commented per-block variant:
+ *   __shared__ val; if (threadIdx.x == 0) val = sum(in, n); __syncthreads();  */
+int oracle_form_block(float* out, const float* in, int64_t n, int mode, uint64_t* adds) {
+  if (n < 0 || (n > 0 && (!out || !in)) || (n > 0 && out == in)) return 1;
+  int64_t G = oracle_grid_blocks(n);
+  for (int64_t b = 0; b < G; ++b) {
+    double val = fig1_sum(in, n, adds); /* thread 0 of block b, then barrier */
+    for (int64_t t = 0; t < FIG1_BLOCK; ++t) {
+      int64_t tid = oracle_tid(b, t, mode);
+      if (tid < n) out[tid] = fig1_div(in[tid], val);
+    }
+  }
+  return 0;
+}
+
+/* Form 3, after parallel LICM: `sum` hoisted before the launch (PAPER.md:117,
+ * 226-230, 592-598).  out == in is allowed under the paper's lock-step reading
+ * (every thread executes instruction k before any thread executes
+ * instruction k+1), so every load of in[tid] precedes every store to out[tid];
+ * the literal index writes an element up to 32 times, so an in-place run reads
+ * from a snapshot of `in` (reading R9). */
+int oracle_form_hoisted(float* out, const float* in, int64_t n, int mode, uint64_t* adds) {
+  if (n < 0 || (n > 0 && (!out || !in))) return 1;
+  if (n == 0) return 0;
+  float* snapshot = NULL;
+  if (out == in) {
+    snapshot = (float*)malloc((size_t)n * sizeof(float));
+    if (!snapshot) return 2;
+    memcpy(snapshot, in, (size_t)n * sizeof(float));
+    in = snapshot;
+  }
+  double val = fig1_sum(in, n, adds);
+  int64_t G = oracle_grid_blocks(n);
+  for (int64_t b = 0; b < G; ++b)
+    for (int64_t t = 0; t < FIG1_BLOCK; ++t) {
+      int64_t tid = oracle_tid(b, t, mode);
+      if (tid < n) out[tid] = fig1_div(in[tid], val);
+    }
+  free(snapshot);
+  return 0;
+}
+
+int oracle_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                int64_t ld_in, int mode) {
+  if (rows < 0 || cols < 0 || ld_out < cols || ld_in < cols) return 1;
+  for (int64_t r = 0; r < rows; ++r) {
+    int rc = oracle_form_hoisted(out + r * ld_out, in + r * ld_in, cols, mode, NULL);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int oracle_replay(float* out, const float* in, int64_t n, int mode, float s) {
+  if (n < 0 || (n > 0 && (!out || !in))) return 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (oracle_is_covered(n, mode, i)) out[i] = in[i] / s; /* binary32 RN */
+  return 0;
+}

@@ -1,0 +1,71 @@
+/*
+ * oracle/norm_oracle.h — CPU oracle for Fig. 1 `normalize` (arxiv 2207.00257).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header or constant with the CUDA path (paper_2207_00257_b200/ and
+ * include/), and the product path never calls it.
+ *
+ * Plain, slow, obviously-correct C in fp64 (plus an exact integer
+ * superaccumulator).  Each function cites the passage it follows.  Readings of
+ * the paper where it is silent/garbled are listed in DESIGN.md §3 (R1..R12).
+ *
+ * Parity status:
+ *   coverage (brute + closed)  pinned: hand-derived golden cases, brute force.
+ *   oracle_sum_exact           pinned: math.fsum, integer closed forms.
+ *   forms thread/block/hoisted pinned: mutual bit agreement, op counts of
+ *                              PAPER.md:117 / SPEC.md:617, 1/n, sum-to-1.
+ *   oracle_replay              pinned: exact rational RN32 via fractions.
+ *   the exact fp32 bits of the GPU divisor s: parity unpinned (any fp32
+ *   within 1e-6 of S is correct; PAPER.md:100 elides `sum`).
+ */
+#ifndef NORM_ORACLE_H
+#define NORM_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORACLE_LITERAL = 0, ORACLE_DENSE = 1 };
+
+/* Fig. 1 launch: normalize<<<(n+31)/32, 32>>>. */
+int64_t oracle_grid_blocks(int64_t n);
+/* Fig. 1 index: tid = blockIdx.x + blockDim.x * threadIdx.x [LITERAL];
+ * the conventional blockIdx.x * blockDim.x + threadIdx.x [DENSE, reading R1]. */
+int64_t oracle_tid(int64_t b, int64_t t, int mode);
+
+/* Enumerate every (blockIdx, threadIdx) of the launch; mult[tid]++ for tid < n. */
+int oracle_coverage_brute(int64_t n, int mode, uint32_t* mult);
+/* Closed form of the covered set C(n).  count = |C(n)|;
+ * prefix_len = L if C(n) == [0, L), else -1. */
+int oracle_coverage_closed(int64_t n, int mode, int64_t* count, int64_t* prefix_len);
+int oracle_is_covered(int64_t n, int mode, int64_t i);
+
+/* Sequential fp64 sum in index order (reading R2 of the elided `sum`). */
+double oracle_sum_seq(const float* x, int64_t n);
+/* Exact sum of the n fp32 values, correctly rounded to fp64 (superaccumulator).
+ * Non-finite classification follows a plain IEEE sum (reading R7). */
+double oracle_sum_exact(const float* x, int64_t n);
+/* Exact sum of |x_i|, correctly rounded to fp64 (tolerance scale for signed inputs). */
+double oracle_sum_abs_exact(const float* x, int64_t n);
+
+/* The three forms of Fig. 1 (PAPER.md:100-114 and caption 117).  out != in is
+ * required for forms 1 and 2 (reading R9); *adds receives the number of
+ * additions performed by `sum` calls.  Return 0 ok, nonzero on bad arguments. */
+int oracle_form_thread(float* out, const float* in, int64_t n, int mode, uint64_t* adds);
+int oracle_form_block(float* out, const float* in, int64_t n, int mode, uint64_t* adds);
+int oracle_form_hoisted(float* out, const float* in, int64_t n, int mode, uint64_t* adds);
+
+/* Batched variant (reading R10): row r == oracle_form_hoisted on row r. */
+int oracle_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                int64_t ld_in, int mode);
+
+/* Replay given a divisor s: out[i] = in[i] / s in binary32 RN for i in C(n). */
+int oracle_replay(float* out, const float* in, int64_t n, int mode, float s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

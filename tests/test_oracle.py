@@ -1,0 +1,328 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and mathematics fix.
+
+Each test pins the oracle to something other than itself:
+  * hand-derived coverage cases from Fig. 1's launch/index (tests/golden/),
+  * brute-force (blockIdx, threadIdx) enumeration vs the closed form,
+  * math.fsum (exact, correctly rounded) and integer closed forms for the sum,
+  * exact rational arithmetic (fractions) for binary32 division,
+  * the op counts of the Fig. 1 caption and SPEC.md:617,
+  * uniform input -> 1/n and sum-to-1 under full coverage (north_star).
+"""
+import json
+import math
+import os
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from conftest import GOLDEN
+
+
+def golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def rn32(q: Fraction) -> np.float32:
+    """Round an exact rational to binary32, nearest-even (IEEE 754), from first principles."""
+    if q == 0:
+        return np.float32(0.0)
+    sign = -1 if q < 0 else 1
+    a = abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    assert Fraction(2) ** e <= a < Fraction(2) ** (e + 1)
+    ulp = Fraction(2) ** max(e - 23, -149)
+    m = a / ulp
+    fl = m.numerator // m.denominator
+    rem = m - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    v = fl * ulp
+    if v >= Fraction(2) ** 128:
+        return np.float32(sign * np.inf)
+    return np.float32(sign * float(v))  # v is a binary32 value: exact in double
+
+
+# ------------------------------------------------------------------ coverage
+
+def test_coverage_golden_small():
+    g = golden("fig1_coverage_small.json")
+    for c in g["cases"]:
+        n = c["n"]
+        assert oracle.grid_blocks(n) == c["G"]
+        mult = oracle.coverage_brute(n, "literal")
+        assert sorted(np.nonzero(mult)[0].tolist()) == c["covered"], n
+        assert set(np.nonzero(oracle.covered_mask(n, "literal"))[0].tolist()) == set(c["covered"])
+        assert oracle.coverage_closed(n, "literal")[0] == len(c["covered"])
+    for c in g["ranges"]:
+        n = c["n"]
+        assert oracle.grid_blocks(n) == c["G"]
+        mult = oracle.coverage_brute(n, "literal")
+        L = c["covered_prefix"]
+        assert np.all(mult[:L] > 0) and np.all(mult[L:] == 0), n
+        for k, v in c["multiplicity"].items():
+            assert mult[int(k)] == v, (n, k)
+        assert oracle.coverage_closed(n, "literal") == (L, L)
+
+
+def test_coverage_survey_counts():
+    for c in golden("survey_coverage_counts.json")["cases"]:
+        assert oracle.coverage_closed(c["n"], "literal")[0] == c["count"]
+        if c["n"] <= (1 << 22):
+            assert int(np.count_nonzero(oracle.coverage_brute(c["n"], "literal"))) == c["count"]
+
+
+def test_tid_expression():
+    # tid = blockIdx.x + blockDim.x * threadIdx.x with blockDim.x = 32.
+    assert oracle.tid(5, 3, "literal") == 5 + 32 * 3
+    assert oracle.tid(5, 3, "dense") == 5 * 32 + 3
+
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_closed_form_equals_brute_force(mode):
+    ns = list(range(0, 5001)) + [random.Random(1).randrange(5000, 1 << 22) for _ in range(40)]
+    for n in ns:
+        mult = oracle.coverage_brute(n, mode)
+        cov = mult > 0
+        count, prefix = oracle.coverage_closed(n, mode)
+        assert count == int(cov.sum()), (n, mode)
+        is_prefix = n == 0 or (cov[:count].all() and not cov[count:].any())
+        assert (prefix >= 0) == is_prefix and (prefix < 0 or prefix == count), (n, mode)
+        if n <= 5000:
+            assert np.array_equal(oracle.covered_mask(n, mode), cov)
+        if mode == "dense":
+            assert np.all(mult == 1)
+        else:
+            assert mult.max(initial=0) <= 32
+
+
+def test_full_coverage_set():
+    # literal index covers every element only for n = 1 and 993 <= n <= 1025
+    full = [n for n in range(1, 5001) if oracle.coverage_closed(n, "literal")[0] == n]
+    assert full == [1] + list(range(993, 1026))
+    for n in (1, 993, 1024, 1025):
+        assert np.all(oracle.coverage_brute(n, "literal") > 0)
+
+
+def test_is_covered_sampled_large():
+    n = 1 << 32
+    L = oracle.coverage_closed(n)[0]
+    for i in (0, 1, L - 1, L, L + 1, n - 1, 2**31, 2**27 + 991):
+        assert oracle.is_covered(n, i) == (i < L)
+    assert not oracle.is_covered(n, n) and not oracle.is_covered(n, -1)
+
+
+# ---------------------------------------------------------------------- sums
+
+def _random_f32_bits(rng, n, allow_subnormal=True):
+    u = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    x = u.view(np.float32)
+    x = np.where(np.isfinite(x), x, np.float32(1.5))
+    if not allow_subnormal:
+        x = np.where(np.abs(x) < np.finfo(np.float32).tiny, np.float32(0.25), x)
+    return x.astype(np.float32)
+
+
+def _fsum(x):
+    return math.fsum(float(v) for v in x)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sum_exact_matches_fsum_random_bits(seed):
+    rng = np.random.default_rng(seed)
+    for n in (1, 2, 3, 17, 1000, 20000):
+        x = _random_f32_bits(rng, n)
+        assert oracle.sum_exact(x) == _fsum(x)
+        assert oracle.sum_abs_exact(x) == _fsum(np.abs(x))
+
+
+@pytest.mark.parametrize("dist", range(5))
+def test_sum_exact_matches_fsum_generator(dist):
+    x = gen.make_host(50000, seed=3, dist=dist)
+    assert oracle.sum_exact(x) == _fsum(x)
+
+
+def test_sum_exact_cancellation_and_subnormals():
+    big = np.float32(3.0e38)
+    x = np.array([big, np.float32(1e-45), -big, np.float32(2**-140)], dtype=np.float32)
+    assert oracle.sum_exact(x) == _fsum(x)  # exact: 2^-149 + 2^-140
+    x = np.array([1.0, 2.0**-60, -1.0], dtype=np.float32)
+    assert oracle.sum_exact(x) == 2.0**-60
+    x = np.array([2.0**100] * 3 + [-(2.0**100)] * 3 + [np.float32(1e-45)], dtype=np.float32)
+    assert oracle.sum_exact(x) == float(np.float32(1e-45))
+
+
+def test_sum_exact_rounding_ties():
+    # 2^53 + 1 is a tie between 2^53 and 2^53 + 2 -> even (2^53); +3 -> 2^53 + 4.
+    x = np.array([2.0**53, 1.0], dtype=np.float32)
+    assert oracle.sum_exact(x) == 2.0**53
+    x = np.array([2.0**53, 1.0, 2.0], dtype=np.float32)
+    assert oracle.sum_exact(x) == 2.0**53 + 4
+    x = np.array([2.0**53, 1.0, 2.0**-20], dtype=np.float32)
+    assert oracle.sum_exact(x) == 2.0**53 + 2  # sticky bit breaks the tie upward
+
+
+def test_sum_closed_forms():
+    for n in (1, 7, 8, 9, 1000, 12345):
+        assert oracle.sum_exact(gen.make_host(n, dist="const")) == n
+        q, r = divmod(n, 8)
+        assert oracle.sum_exact(gen.make_host(n, dist="ramp")) == 36 * q + r * (r + 1) // 2
+    # unit grid: values are k * 2^-24 with integer k -> exact integer sum
+    x = gen.make_host(100003, seed=9, dist="unit")
+    k = sum(int(v) for v in (x.astype(np.float64) * 2**24))
+    assert oracle.sum_exact(x) == float(Fraction(k, 2**24))
+    assert oracle.sum_exact(np.array([1, 2, 3, 4, 5, 6, 7, 8], np.float32)) == 36
+
+
+def test_sum_nonfinite_classification():
+    inf, nan = np.float32(np.inf), np.float32(np.nan)
+    assert oracle.sum_exact(np.array([1, inf, 2], np.float32)) == np.inf
+    assert oracle.sum_exact(np.array([1, -inf], np.float32)) == -np.inf
+    assert math.isnan(oracle.sum_exact(np.array([inf, -inf], np.float32)))
+    assert math.isnan(oracle.sum_exact(np.array([1, nan], np.float32)))
+    z = oracle.sum_exact(np.array([-0.0, -0.0], np.float32))
+    assert z == 0 and math.copysign(1, z) == -1
+    z = oracle.sum_exact(np.array([-0.0, 0.0], np.float32))
+    assert z == 0 and math.copysign(1, z) == 1
+    assert oracle.sum_exact(np.zeros(0, np.float32)) == 0
+
+
+def test_sum_seq_is_index_order_double():
+    x = np.array([1.0, 2.0**-53, 2.0**-53], dtype=np.float32)
+    assert oracle.sum_seq(x) == 1.0  # each tiny add rounds away in fp64
+    assert oracle.sum_exact(x) == 1.0 + 2.0**-52
+
+
+# --------------------------------------------------------------------- forms
+
+FORM_NS = [1, 8, 31, 32, 33, 100, 992, 993, 1024, 1025, 1026, 2048, 4099]
+
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+@pytest.mark.parametrize("dist", range(5))
+def test_three_forms_agree_bitwise(mode, dist):
+    for n in FORM_NS:
+        x = gen.make_host(n, seed=dist + 11, dist=dist)
+        sentinel = np.full(n, np.nan, dtype=np.float32)
+        o1, a1 = oracle.form_thread(x, mode, sentinel.copy())
+        o2, a2 = oracle.form_block(x, mode, sentinel.copy())
+        o3, a3 = oracle.form_hoisted(x, mode, sentinel.copy())
+        assert o1.tobytes() == o2.tobytes() == o3.tobytes(), (n, mode, dist)
+        G = oracle.grid_blocks(n)
+        assert (a1, a2, a3) == (32 * G * n, G * n, n)
+        cov = oracle.covered_mask(n, mode)
+        assert np.all(np.isnan(o3[~cov]))  # untouched (sentinel kept)
+        assert not np.any(np.isnan(o3[cov]))
+
+
+def test_opcounts_golden():
+    for c in golden("fig1_opcounts.json")["cases"]:
+        x = gen.make_host(c["n"], dist="unit")
+        assert oracle.form_thread(x)[1] == c["thread"]
+        assert oracle.form_block(x)[1] == c["block"]
+        assert oracle.form_hoisted(x)[1] == c["hoisted"]
+
+
+def test_spec_n8_golden():
+    g = golden("spec_n8.json")
+    x = np.array(g["in"], dtype=np.float32)
+    dense = oracle.normalize(x, "dense")
+    for i, q in enumerate(g["dense_out"]):
+        assert dense[i] == rn32(Fraction(q))
+    lit = oracle.normalize(x, "literal", out=np.full(8, -7.0, np.float32))
+    assert lit[0] == rn32(Fraction(g["literal_written"]["0"]))
+    assert np.all(lit[1:] == -7.0)
+
+
+@pytest.mark.parametrize("n", [1, 3, 64, 1000, 4096, 1 << 20])
+def test_uniform_input_gives_one_over_n(n):
+    out = oracle.normalize(np.ones(n, np.float32), "dense")
+    assert np.all(out == rn32(Fraction(1, n)))
+
+
+def test_sum_to_one_full_coverage():
+    for mode, n in [("dense", 100003), ("dense", 1 << 16), ("literal", 1000), ("literal", 1025)]:
+        x = gen.make_host(n, seed=5, dist="unit")
+        out = oracle.normalize(x, mode)
+        assert abs(math.fsum(out.astype(np.float64)) - 1.0) <= 1e-6
+
+
+def test_partial_coverage_invariant():
+    # sum over C(n) of out == sum over C(n) of in / S (north_star invariant, reading R11)
+    n = (1 << 20) + 7
+    x = gen.make_host(n, seed=2, dist="unit")
+    out = oracle.normalize(x, "literal")
+    cov = oracle.covered_mask(n)
+    S = oracle.sum_exact(x)
+    lhs = math.fsum(out[cov].astype(np.float64))
+    rhs = math.fsum(x[cov].astype(np.float64)) / S
+    assert abs(lhs - rhs) <= 1e-6 * rhs
+
+
+def test_hoisted_in_place_and_forms_reject_alias():
+    x = gen.make_host(3000, seed=4, dist="wide")
+    ref = oracle.normalize(x, "literal", out=x.copy())
+    y = x.copy()
+    oracle.form_hoisted(y, "literal", out=y)  # out == in (reading R9)
+    assert y.tobytes() == ref.tobytes()
+    with pytest.raises(ValueError):
+        oracle.form_thread(y, "literal", out=y)
+    with pytest.raises(ValueError):
+        oracle.form_block(y, "literal", out=y)
+
+
+def test_hoisted_matches_exact_quotient():
+    # out[i] is RN32(in[i] / S) up to double rounding: within 1 ulp, and exact rational check
+    x = gen.make_host(777, seed=8, dist="wide")
+    out = oracle.normalize(x, "dense")
+    S = Fraction(_fsum(x))
+    for i in range(0, 777, 37):
+        exact = Fraction(float(x[i])) / S
+        assert abs(Fraction(float(out[i])) - exact) <= abs(exact) * Fraction(1, 2**23)
+
+
+# -------------------------------------------------------------------- replay
+
+def test_replay_is_ieee_binary32_division():
+    rng = np.random.default_rng(0)
+    x = _random_f32_bits(rng, 3000)
+    for s in (np.float32(3.0), np.float32(1e-30), np.float32(7.123e20), np.float32(-0.37),
+              np.float32(2.0**-126), np.float32(1e38)):
+        out = oracle.replay(x, s, "dense")
+        for i in range(0, 3000, 7):
+            assert out[i].tobytes() == rn32(Fraction(float(x[i])) / Fraction(float(s))).tobytes() \
+                or (out[i] == 0 and rn32(Fraction(float(x[i])) / Fraction(float(s))) == 0)
+
+
+def test_replay_special_divisors():
+    x = np.array([1.0, -2.0, 0.0, np.inf], np.float32)
+    assert np.array_equal(oracle.replay(x, np.float32(np.inf), "dense")[:3], [0, -0.0, 0])
+    o = oracle.replay(x, np.float32(0.0), "dense")
+    assert o[0] == np.inf and o[1] == -np.inf and np.isnan(o[2]) and o[3] == np.inf
+
+
+def test_replay_respects_coverage():
+    n = 100
+    x = gen.make_host(n, dist="ramp")
+    out = oracle.replay(x, np.float32(2.0), "literal", out=np.full(n, -1, np.float32))
+    cov = oracle.covered_mask(n)
+    assert np.all(out[~cov] == -1) and np.all(out[cov] == x[cov] / np.float32(2.0))
+
+
+# ---------------------------------------------------------------------- rows
+
+def test_rows_oracle():
+    R, C = 5, 4096
+    x = np.stack([gen.make_host(C, seed=r, dist="unit") for r in range(R)])
+    out = oracle.rows(x, "literal", out=np.full((R, C), -3.0, np.float32))
+    for r in range(R):
+        assert out[r].tobytes() == oracle.normalize(x[r], "literal", out=np.full(C, -3.0, np.float32)).tobytes()
+    assert np.all(out[:, 1120:] == -3.0)  # |C(4096)| = 1120
+    ones = oracle.rows(np.ones((3, 64), np.float32), "dense")
+    assert np.all(ones == rn32(Fraction(1, 64)))
