@@ -1,0 +1,193 @@
+/*
+ * include/libnorm.h — C ABI of libnorm: Fig. 1 `normalize` of arxiv 2207.00257
+ * ("High-Performance GPU-to-CPU Transpilation and Optimization via High-Level
+ * Parallel Constructs") after parallel loop-invariant code motion, on B200
+ * (sm_100a).
+ *
+ * The operation (Fig. 1, and §2.1):
+ *
+ *     __global__ void normalize(float *out, float* in, int n) {
+ *       int tid = blockIdx.x + blockDim.x * threadIdx.x;
+ *       float val = sum(in, n);
+ *       if (tid < n) out[tid] = in[tid] / val;
+ *     }
+ *     void launch(... d_out, ... d_in, int n) {
+ *       normalize<<<(n+31)/32, 32>>>(d_out, d_in, n);
+ *     }
+ *
+ * with `sum` (elided at PAPER.md:100) hoisted out of the kernel by parallel LICM
+ * (PAPER.md:117, 592-598), so every call is:  S = sum_{i<n} in[i] (one global
+ * reduction over ALL n elements), then out[i] = in[i] / s for every i in the
+ * covered set C(n) of the launch, where s is an fp32 within 1e-6 relative of S.
+ * Elements outside C(n) are left untouched.
+ *
+ * Coverage C(n), G = ceil(n/32):
+ *   NORM_INDEX_LITERAL (default; tid = b + 32 t as printed at PAPER.md:103):
+ *       G >= 32: C(n) = [0, min(n, G + 992))
+ *       G <  32: C(n) = { x < n : x mod 32 < G }
+ *   NORM_INDEX_DENSE (tid = 32 b + t, the caption's "normalizes a vector"):
+ *       C(n) = [0, n)
+ * The readings taken where the paper is silent are DESIGN.md §3 (R1..R15).
+ *
+ * Conventions for every entry point:
+ *   - returns norm_status_t; never aborts, throws or prints.  norm_last_error()
+ *     returns a thread-local detail string for the last failing call.
+ *   - device entries are stream-ordered and return after enqueue, like the
+ *     kernel launch of Fig. 1; asynchronous device faults surface at the
+ *     caller's next synchronisation.  They never synchronise the device.
+ *   - the caller owns all memory it passes (in, out, sum_out*, workspace);
+ *     libnorm never frees caller memory.  Pointers are device pointers unless
+ *     the name says `host`.  Float pointers must be 4-byte aligned.
+ *   - `out == in` (exact alias) is allowed (reading R9: all loads of `in`
+ *     precede every store under the paper's lock-step semantics);
+ *     partial overlap returns NORM_ERR_OVERLAP.
+ *   - n == 0 (or rows == 0 / cols == 0) is a no-op returning NORM_OK (R8).
+ *   - a zero or non-finite sum is not an error: IEEE results (R7).
+ *   - results are bitwise deterministic run to run for the same arguments
+ *     (same n, index mode, path, pointer alignment mod 32 B and world size).
+ */
+#ifndef LIBNORM_H
+#define LIBNORM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LIBNORM_VERSION_MAJOR 0
+#define LIBNORM_VERSION_MINOR 1
+
+typedef enum {
+  NORM_OK = 0,
+  NORM_ERR_INVALID_VALUE = 1, /* n < 0, NULL with work to do, misaligned, bad enum, ld < cols */
+  NORM_ERR_OVERLAP = 2,       /* out and in overlap without being identical */
+  NORM_ERR_CUDA = 3,          /* CUDA runtime / launch error (detail in norm_last_error) */
+  NORM_ERR_NCCL = 4,          /* NCCL error */
+  NORM_ERR_WORKSPACE = 5,     /* caller workspace too small, or device allocation failed */
+  NORM_ERR_UNSUPPORTED = 6    /* not an sm_100 device, or literal grid > 2^31-1 blocks */
+} norm_status_t;
+
+typedef enum {
+  NORM_INDEX_LITERAL = 0, /* Fig. 1 as printed: tid = blockIdx.x + blockDim.x*threadIdx.x */
+  NORM_INDEX_DENSE = 1    /* tid = blockIdx.x*blockDim.x + threadIdx.x: all of [0, n)      */
+} norm_index_t;
+
+typedef enum {
+  NORM_PATH_AUTO = 0,     /* small: one CTA; covered bytes fit L2: fused; else two-pass   */
+  NORM_PATH_TWO_PASS = 1, /* reduce kernel, then scale kernel (PDL-chained)               */
+  NORM_PATH_FUSED = 2,    /* one cooperative kernel: reduce, grid barrier, scale from L2  */
+  NORM_PATH_SMALL = 3     /* one CTA does everything (any n; intended for n <= 2^15)       */
+} norm_path_t;
+
+typedef struct {
+  void* stream;         /* cudaStream_t to enqueue on; NULL = legacy default stream       */
+  int32_t index;        /* norm_index_t, default NORM_INDEX_LITERAL                        */
+  int32_t path;         /* norm_path_t, default NORM_PATH_AUTO                             */
+  float* sum_out;       /* optional device ptr: receives s, the fp32 divisor used.
+                           norm_rows: array of `rows` floats, one divisor per row          */
+  double* sum_out_f64;  /* optional device ptr: receives S as accumulated (fp64).
+                           norm_rows: array of `rows` doubles                              */
+  void* workspace;      /* optional caller-owned device scratch (>= norm_workspace_bytes),
+                           zero-filled before its first use; libnorm leaves it reusable.
+                           NULL = an internal cache keyed by (device, stream).  Calls that
+                           may run concurrently must not share a workspace.                */
+  size_t workspace_bytes;
+  void* ev_reduce_begin; /* optional cudaEvent_t recorded just before / after the reduce  */
+  void* ev_reduce_end;   /* kernel on `stream` (bench instrumentation); NULL = none        */
+} norm_opts_t;
+
+/* Designated defaults: literal index, AUTO path, default stream, no outputs. */
+#define NORM_OPTS_INIT {NULL, NORM_INDEX_LITERAL, NORM_PATH_AUTO, NULL, NULL, NULL, 0, NULL, NULL}
+
+/* ---------------------------------------------------------------- vector */
+
+/* Fig. 1 `launch(d_out, d_in, n)` after LICM: literal index,
+ * legacy default stream, AUTO path.  out, in: device fp32[n]. */
+norm_status_t norm_launch(float* out, const float* in, int64_t n);
+
+/* As norm_launch with options (NULL o = NORM_OPTS_INIT). */
+norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, const norm_opts_t* o);
+
+/* End-to-end variant on HOST buffers: out_host/in_host are host fp32[n] (pinned
+ * memory gives asynchronous, overlapped copies; pageable memory works but the
+ * copies serialise).  libnorm streams `in` to the device in chunks, reduces each
+ * chunk as it lands, keeps only the covered elements resident, scales them and
+ * copies back only out_host[C(n)] — uncovered host outputs are untouched.
+ * Enqueued on o->stream; the caller synchronises that stream before reading
+ * out_host.  o->workspace is ignored (device staging is internal, per stream).
+ * Same s bit-for-bit as long as the chunk partition is unchanged. */
+norm_status_t norm_launch_host(float* out_host, const float* in_host, int64_t n,
+                               const norm_opts_t* o);
+
+/* ------------------------------------------------------------------ rows */
+
+/* Batched per-row variant (reading R10; BASELINE configs[4]): for each row r,
+ * out[r*ld_out + i] = in[r*ld_in + i] / s_r for i in C(cols), s_r ~ sum of row r.
+ * Row r is exactly norm_launch_ex(out + r*ld_out, in + r*ld_in, cols, o).
+ * o->sum_out / sum_out_f64, when set, receive one value per row. */
+norm_status_t norm_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                        int64_t ld_out, int64_t ld_in, const norm_opts_t* o);
+
+/* ------------------------------------------------------------ host-only */
+
+/* Size of C(n) for the index mode; *prefix_len = L if C(n) == [0, L), else -1.
+ * Pure host function (no CUDA call). */
+norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* prefix_len);
+
+/* Bytes of device workspace a call with (n, o) needs if the caller supplies one. */
+norm_status_t norm_workspace_bytes(int64_t n, const norm_opts_t* o, size_t* bytes);
+
+/* Algorithmic HBM bytes of one call (the roofline numerator):
+ * two-pass 4n + 8|C(n)|.  Pure host function. */
+norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t* bytes);
+
+/* --------------------------------------------------------- multi-GPU (NCCL) */
+
+/* Opaque: owns an ncclComm_t on the device current at init, plus device scratch
+ * for the per-rank partial sums. One process per GPU. */
+typedef struct norm_comm norm_comm_t;
+
+/* Global index ranges owned by one rank, in ascending order.  The rank's local
+ * buffers hold its ranges concatenated in this order. */
+typedef struct {
+  int32_t nranges;  /* 0, 1 or 2 */
+  int64_t begin[2];
+  int64_t len[2];
+} norm_shard_t;
+
+/* Rank 0 creates the NCCL unique id (128 bytes); the caller broadcasts it
+ * (the Python binding uses the torch.distributed store). */
+norm_status_t norm_comm_unique_id(unsigned char id[128]);
+/* Collective over all `world` ranks; binds to the current CUDA device. */
+norm_status_t norm_comm_init(norm_comm_t** comm, int32_t world, int32_t rank,
+                             const unsigned char id[128]);
+norm_status_t norm_comm_destroy(norm_comm_t* comm);
+
+/* Partition [0, n) over `world` ranks (pure host function; plan[world]).
+ * DENSE, or coverage_balanced == 0: one contiguous range per rank, boundaries
+ * rounded to 8 elements.  LITERAL with coverage_balanced != 0 and a prefix
+ * coverage [0, L): each rank gets a slice of [0, L) and a slice of [L, n), so
+ * the post-collective scale work is balanced. */
+norm_status_t norm_plan_shards(int64_t n, int32_t world, int32_t index,
+                               int32_t coverage_balanced, norm_shard_t* plan);
+
+/* Sharded normalize of a global vector of n_global elements: every rank calls it
+ * with its own shard `mine` (from norm_plan_shards) and local buffers
+ * in_local/out_local of sum(mine->len) elements.  Local reduce -> one NCCL
+ * all-gather of an 8-byte partial per rank on o->stream -> fixed rank-order
+ * combine (identical s on every rank) -> scale of the locally covered elements.
+ * o->index selects the coverage of the GLOBAL index. */
+norm_status_t norm_launch_sharded(norm_comm_t* comm, float* out_local, const float* in_local,
+                                  const norm_shard_t* mine, int64_t n_global,
+                                  const norm_opts_t* o);
+
+/* -------------------------------------------------------------- errors */
+const char* norm_status_string(norm_status_t s);
+const char* norm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBNORM_H */

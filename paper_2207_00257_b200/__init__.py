@@ -1,0 +1,34 @@
+"""libnorm — Fig. 1 `normalize` of arxiv 2207.00257 on B200 (sm_100a).
+
+Thin ctypes binding over the C ABI in ``include/libnorm.h`` (argument
+marshalling only: every step of the path runs in the CUDA kernels of
+``libnorm.so``).  PyTorch supplies device memory, the current stream and the
+process group; nothing here computes on the CPU, and there is no fallback:
+if ``libnorm.so`` is missing or the device is not sm_100, calls raise.
+
+    out[i] = in[i] / sum(in)   for i in the covered set C(n) of the launch
+    normalize<<<(n+31)/32, 32>>> with tid = blockIdx.x + blockDim.x*threadIdx.x
+    (PAPER.md:98-119); uncovered outputs are untouched.
+"""
+from ._lib import (  # noqa: F401
+    Comm,
+    NormError,
+    algorithmic_bytes,
+    coverage,
+    last_error,
+    lib,
+    normalize,
+    normalize_host,
+    normalize_rows,
+    plan_shards,
+    status_string,
+    workspace_bytes,
+    INDEX,
+    PATH,
+)
+
+__all__ = [
+    "normalize", "normalize_rows", "normalize_host", "coverage", "algorithmic_bytes",
+    "plan_shards", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
+    "last_error", "INDEX", "PATH",
+]

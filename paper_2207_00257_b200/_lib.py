@@ -1,0 +1,252 @@
+"""ctypes marshalling for libnorm.so (see include/libnorm.h for semantics)."""
+import ctypes
+import os
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_DIR, "libnorm.so")
+
+INDEX = {"literal": 0, "dense": 1}
+PATH = {"auto": 0, "two_pass": 1, "fused": 2, "small": 3}
+STATUS = ["NORM_OK", "NORM_ERR_INVALID_VALUE", "NORM_ERR_OVERLAP", "NORM_ERR_CUDA",
+          "NORM_ERR_NCCL", "NORM_ERR_WORKSPACE", "NORM_ERR_UNSUPPORTED"]
+
+
+class NormOpts(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_void_p), ("index", ctypes.c_int32), ("path", ctypes.c_int32),
+                ("sum_out", ctypes.c_void_p), ("sum_out_f64", ctypes.c_void_p),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("ev_reduce_begin", ctypes.c_void_p), ("ev_reduce_end", ctypes.c_void_p)]
+
+
+class NormShard(ctypes.Structure):
+    _fields_ = [("nranges", ctypes.c_int32), ("begin", ctypes.c_int64 * 2),
+                ("len", ctypes.c_int64 * 2)]
+
+    def ranges(self):
+        return [(self.begin[k], self.len[k]) for k in range(self.nranges)]
+
+
+class NormError(RuntimeError):
+    def __init__(self, status, detail):
+        self.status = status
+        name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{name}: {detail}")
+
+
+_lib = None
+
+
+def lib():
+    """Load libnorm.so (built in-tree by `make` / __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} is missing: build it with `make` (no CPU fallback exists)")
+        L = ctypes.CDLL(_SO)
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+        optp = ctypes.POINTER(NormOpts)
+        sig = {
+            "norm_launch": [vp, vp, i64],
+            "norm_launch_ex": [vp, vp, i64, optp],
+            "norm_launch_host": [vp, vp, i64, optp],
+            "norm_rows": [vp, vp, i64, i64, i64, i64, optp],
+            "norm_coverage": [i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "norm_workspace_bytes": [i64, optp, ctypes.POINTER(ctypes.c_size_t)],
+            "norm_algorithmic_bytes": [i64, i32, ctypes.POINTER(i64)],
+            "norm_comm_unique_id": [ctypes.c_char_p],
+            "norm_comm_init": [ctypes.POINTER(vp), i32, i32, ctypes.c_char_p],
+            "norm_comm_destroy": [vp],
+            "norm_plan_shards": [i64, i32, i32, i32, ctypes.POINTER(NormShard)],
+            "norm_launch_sharded": [vp, vp, vp, ctypes.POINTER(NormShard), i64, optp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.norm_status_string.argtypes = [ctypes.c_int]
+        L.norm_status_string.restype = ctypes.c_char_p
+        L.norm_last_error.argtypes = []
+        L.norm_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def status_string(s):
+    return lib().norm_status_string(s).decode()
+
+
+def last_error():
+    return lib().norm_last_error().decode()
+
+
+def _check(st):
+    if st != 0:
+        raise NormError(st, last_error())
+
+
+def _enum(table, v):
+    return table[v] if isinstance(v, str) else int(v)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(stream, device=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _opts(index, path, stream, sum_out, sum_out_f64, workspace=None, events=None, device=None):
+    o = NormOpts()
+    o.stream = _stream_handle(stream, device)
+    o.index = _enum(INDEX, index)
+    o.path = _enum(PATH, path)
+    o.sum_out = _ptr(sum_out)
+    o.sum_out_f64 = _ptr(sum_out_f64)
+    if workspace is not None:
+        o.workspace = workspace.data_ptr()
+        o.workspace_bytes = workspace.numel() * workspace.element_size()
+    if events is not None:
+        o.ev_reduce_begin = events[0].cuda_event
+        o.ev_reduce_end = events[1].cuda_event
+    return o
+
+
+def _check_f32(t, name, cuda=True):
+    import torch
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    if cuda and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
+def normalize(out, inp, index="literal", path="auto", stream=None, sum_out=None,
+              sum_out_f64=None, workspace=None, events=None):
+    """out[C(n)] = inp[C(n)] / sum(inp) on the GPU (norm_launch_ex).  Returns out.
+
+    out, inp: contiguous float32 CUDA tensors of equal numel (out may be inp).
+    sum_out / sum_out_f64: optional 1-element float32 / float64 CUDA tensors.
+    events: optional (begin, end) torch.cuda.Event pair recorded around the reduce kernel.
+    """
+    _check_f32(out, "out")
+    _check_f32(inp, "inp")
+    if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
+        raise ValueError("out and inp must be contiguous with equal numel")
+    o = _opts(index, path, stream, sum_out, sum_out_f64, workspace, events, inp.device)
+    _check(lib().norm_launch_ex(out.data_ptr(), inp.data_ptr(), inp.numel(), ctypes.byref(o)))
+    return out
+
+
+def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):
+    """Row-wise normalize of 2-D float32 CUDA tensors (unit column stride)."""
+    _check_f32(out, "out")
+    _check_f32(inp, "inp")
+    if out.dim() != 2 or inp.dim() != 2 or out.shape != inp.shape:
+        raise ValueError("out and inp must be 2-D with equal shapes")
+    if (out.shape[1] > 1 and (out.stride(1) != 1 or inp.stride(1) != 1)):
+        raise ValueError("rows must have unit column stride")
+    rows, cols = inp.shape
+    o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=inp.device)
+    _check(lib().norm_rows(out.data_ptr(), inp.data_ptr(), rows, cols, out.stride(0),
+                           inp.stride(0), ctypes.byref(o)))
+    return out
+
+
+def normalize_host(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):
+    """End-to-end entry on HOST buffers (norm_launch_host): CPU float32 tensors or numpy
+    arrays (pin them for overlapped copies).  Enqueued on `stream`; synchronise it
+    before reading `out`."""
+    import numpy as np
+
+    def hp(a):
+        if isinstance(a, np.ndarray):
+            assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+            return a.ctypes.data, a.size
+        _check_f32(a, "host buffer", cuda=False)
+        assert not a.is_cuda and a.is_contiguous()
+        return a.data_ptr(), a.numel()
+
+    po, no = hp(out)
+    pi, ni = hp(inp)
+    if no != ni:
+        raise ValueError("size mismatch")
+    o = _opts(index, "auto", stream, sum_out, sum_out_f64)
+    _check(lib().norm_launch_host(po, pi, ni, ctypes.byref(o)))
+    return out
+
+
+def coverage(n, index="literal"):
+    """(|C(n)|, prefix_len or -1) — host-only."""
+    c, p = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().norm_coverage(n, _enum(INDEX, index), ctypes.byref(c), ctypes.byref(p)))
+    return c.value, p.value
+
+
+def algorithmic_bytes(n, index="literal"):
+    """4n + 8|C(n)|: the roofline numerator of one call — host-only."""
+    b = ctypes.c_int64()
+    _check(lib().norm_algorithmic_bytes(n, _enum(INDEX, index), ctypes.byref(b)))
+    return b.value
+
+
+def workspace_bytes(n=0):
+    b = ctypes.c_size_t()
+    _check(lib().norm_workspace_bytes(n, None, ctypes.byref(b)))
+    return b.value
+
+
+def plan_shards(n, world, index="literal", coverage_balanced=True):
+    """List (per rank) of [(begin, len), ...] global ranges — host-only."""
+    plan = (NormShard * world)()
+    _check(lib().norm_plan_shards(n, world, _enum(INDEX, index), int(bool(coverage_balanced)), plan))
+    return [p.ranges() for p in plan]
+
+
+def _shard_struct(ranges):
+    s = NormShard()
+    s.nranges = len(ranges)
+    for k, (b, ln) in enumerate(ranges):
+        s.begin[k] = b
+        s.len[k] = ln
+    return s
+
+
+class Comm:
+    """NCCL communicator for norm_launch_sharded (one process per GPU).
+
+    The 128-byte NCCL unique id is created on rank 0 and broadcast through the
+    torch.distributed process group (any backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib().norm_comm_unique_id(uid))
+        obj = [bytes(uid.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib().norm_comm_init(ctypes.byref(h), self.world, self.rank, uid))
+        self._h = h
+
+    def normalize_sharded(self, out_local, in_local, ranges, n_global, index="literal",
+                          stream=None, sum_out=None, sum_out_f64=None, events=None):
+        _check_f32(out_local, "out_local")
+        _check_f32(in_local, "in_local")
+        shard = _shard_struct(ranges)
+        if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
+            raise ValueError("local buffers must hold exactly the shard's elements")
+        o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
+        _check(lib().norm_launch_sharded(self._h, out_local.data_ptr(), in_local.data_ptr(),
+                                         ctypes.byref(shard), n_global, ctypes.byref(o)))
+        return out_local
+
+    def destroy(self):
+        if self._h:
+            _check(lib().norm_comm_destroy(self._h))
+            self._h = None

@@ -1,0 +1,205 @@
+// comm.cpp — multi-GPU layer of libnorm: NCCL communicator, shard planner and the
+// sharded normalize (one process per GPU, NVLink 5 / NVSwitch).
+//
+// The method's only cross-GPU exchange is the hoisted `sum`:
+// each rank reduces its shard to an fp64 partial S_k (8 bytes), one ncclAllGather
+// gives every rank all W partials, and the scale kernel's prologue combines them
+// in rank order — an all-reduce whose order is pinned, so every rank divides by
+// bit-identical s, run after run.  An 8-byte message is pure latency, so NCCL's
+// LL protocol is the right tool; there is nothing to overlap it with because the
+// scale cannot start before s exists.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <string>
+
+#include "libnorm.h"
+#include "norm_internal.h"
+
+#define NORM_API extern "C" __attribute__((visibility("default")))
+
+using namespace lnorm;
+
+struct norm_comm {
+  ncclComm_t nccl = nullptr;
+  int world = 0, rank = 0, device = -1;
+  double* send = nullptr;  // [1] this rank's partial
+  double* recv = nullptr;  // [world] all partials, rank order
+  void* ws = nullptr;      // reduce workspace (zeroed)
+};
+
+static norm_status_t nccl_fail(ncclResult_t r, const char* what) {
+  return fail(NORM_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+NORM_API norm_status_t norm_comm_unique_id(unsigned char id[128]) {
+  if (!id) return fail(NORM_ERR_INVALID_VALUE, "id is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(id, &u, 128);
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_comm_init(norm_comm_t** comm, int32_t world, int32_t rank,
+                                      const unsigned char id[128]) {
+  if (!comm || !id || world < 1 || rank < 0 || rank >= world)
+    return fail(NORM_ERR_INVALID_VALUE, "bad comm arguments");
+  *comm = nullptr;
+  norm_comm* c = new norm_comm();
+  c->world = world;
+  c->rank = rank;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaGetDevice");
+  }
+  const size_t bytes = 256 + (size_t)world * sizeof(double);
+  char* buf = nullptr;
+  if ((e = cudaMalloc(&buf, bytes + workspace_bytes())) != cudaSuccess) {
+    delete c;
+    cudaGetLastError();
+    return fail(NORM_ERR_WORKSPACE, "comm scratch cudaMalloc failed");
+  }
+  cudaMemset(buf, 0, bytes + workspace_bytes());
+  c->send = reinterpret_cast<double*>(buf);
+  c->recv = reinterpret_cast<double*>(buf + 256);
+  c->ws = buf + ((bytes + 255) / 256) * 256;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  if (r != ncclSuccess) {
+    cudaFree(buf);
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  *comm = c;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_comm_destroy(norm_comm_t* c) {
+  if (!c) return NORM_OK;
+  norm_status_t s = NORM_OK;
+  if (c->nccl) {
+    ncclResult_t r = ncclCommDestroy(c->nccl);
+    if (r != ncclSuccess) s = nccl_fail(r, "ncclCommDestroy");
+  }
+  cudaFree(c->send);
+  delete c;
+  return s;
+}
+
+static int64_t round8(int64_t x) { return (x / 8) * 8; }
+
+// Slice [lo, hi) into `world` contiguous pieces whose lengths (except the last)
+// are multiples of 8 elements, so each piece keeps the 32-byte phase of `lo`.
+static void split(int64_t lo, int64_t hi, int world, int k, int64_t* b, int64_t* e) {
+  const int64_t len = hi - lo;
+  *b = k == 0 ? lo : lo + round8(len * k / world);
+  *e = k == world - 1 ? hi : lo + round8(len * (k + 1) / world);
+  if (*e < *b) *e = *b;
+}
+
+NORM_API norm_status_t norm_plan_shards(int64_t n, int32_t world, int32_t index,
+                                        int32_t coverage_balanced, norm_shard_t* plan) {
+  if (n < 0 || world < 1 || !plan) return fail(NORM_ERR_INVALID_VALUE, "bad plan arguments");
+  if (index != NORM_INDEX_LITERAL && index != NORM_INDEX_DENSE)
+    return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
+  const Coverage cov = coverage_of(n, index);
+  const bool two = coverage_balanced && index == NORM_INDEX_LITERAL && cov.kind == COV_PREFIX &&
+                   cov.L < n && world > 1;
+  for (int k = 0; k < world; ++k) {
+    norm_shard_t& p = plan[k];
+    memset(&p, 0, sizeof p);
+    int64_t b, e;
+    if (two) {
+      split(0, cov.L, world, k, &b, &e);
+      if (e > b) { p.begin[p.nranges] = b; p.len[p.nranges] = e - b; p.nranges++; }
+      split(cov.L, n, world, k, &b, &e);
+      if (e > b) { p.begin[p.nranges] = b; p.len[p.nranges] = e - b; p.nranges++; }
+    } else {
+      split(0, n, world, k, &b, &e);
+      if (e > b) { p.begin[0] = b; p.len[0] = e - b; p.nranges = 1; }
+    }
+  }
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, const float* in_local,
+                                           const norm_shard_t* mine, int64_t n_global,
+                                           const norm_opts_t* o) {
+  static const norm_opts_t kDef = NORM_OPTS_INIT;
+  if (!o) o = &kDef;
+  if (!c || !mine) return fail(NORM_ERR_INVALID_VALUE, "comm or shard is NULL");
+  if (o->index != NORM_INDEX_LITERAL && o->index != NORM_INDEX_DENSE)
+    return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
+  if (n_global < 0 || mine->nranges < 0 || mine->nranges > 2)
+    return fail(NORM_ERR_INVALID_VALUE, "bad shard");
+  int64_t local = 0, prev_end = 0;
+  for (int k = 0; k < mine->nranges; ++k) {
+    if (mine->len[k] < 0 || mine->begin[k] < prev_end || mine->begin[k] + mine->len[k] > n_global)
+      return fail(NORM_ERR_INVALID_VALUE, "shard ranges must be ascending, disjoint, inside [0, n)");
+    prev_end = mine->begin[k] + mine->len[k];
+    local += mine->len[k];
+  }
+  if (local > 0) {
+    if (!out_local || !in_local) return fail(NORM_ERR_INVALID_VALUE, "NULL local buffer");
+    if ((reinterpret_cast<uintptr_t>(out_local) | reinterpret_cast<uintptr_t>(in_local)) & 3u)
+      return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+    uintptr_t a = reinterpret_cast<uintptr_t>(out_local), b = reinterpret_cast<uintptr_t>(in_local);
+    if (a != b && a < b + local * 4 && b < a + local * 4)
+      return fail(NORM_ERR_OVERLAP, "out_local and in_local partially overlap");
+  }
+  const Coverage cov = coverage_of(n_global, o->index);
+  if (o->index == NORM_INDEX_LITERAL && cov.G > 2147483647LL)
+    return fail(NORM_ERR_UNSUPPORTED, "literal launch needs > 2^31-1 blocks");
+  DeviceInfo d;
+  std::string err;
+  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if (d.device != c->device) return fail(NORM_ERR_INVALID_VALUE, "current device != comm device");
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Workspace ws = workspace_carve(c->ws);
+
+  // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
+  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  cudaError_t e = launch_reduce(in_local, local, ws, c->send, reduce_grid(d, local), st);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  // 2. exchange: W x 8 bytes over NVLink
+  ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  // 3. scale the locally covered elements; the prologue combines recv[0..W) in rank order
+  float* so = o->sum_out;
+  double* so64 = o->sum_out_f64;
+  int64_t off = 0;
+  bool launched = false;
+  for (int k = 0; k < mine->nranges; ++k) {
+    const int64_t gb = mine->begin[k], len = mine->len[k];
+    if (cov.kind == COV_PREFIX) {
+      int64_t ce = gb + len < cov.L ? gb + len : cov.L;
+      int64_t clen = ce > gb ? ce - gb : 0;
+      if (clen > 0) {
+        e = launch_scale(out_local + off, in_local + off, clen, c->recv, c->world, so, so64, d, false, st);
+        if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
+        so = nullptr;
+        so64 = nullptr;
+        launched = true;
+      }
+    } else if (cov.kind == COV_RESIDUE && len > 0) {
+      e = launch_scale_residue(out_local + off, in_local + off, len, gb, cov.G, c->recv, c->world,
+                               so, so64, false, st);
+      if (e != cudaSuccess) return cuda_fail(e, "scale_residue launch");
+      so = nullptr;
+      so64 = nullptr;
+      launched = true;
+    }
+    off += len;
+  }
+  if (!launched && (so || so64)) {  // nothing covered here, but the caller wants s
+    e = launch_scale(out_local, in_local, 0, c->recv, c->world, so, so64, d, false, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
+  }
+  return NORM_OK;
+}

@@ -1,0 +1,433 @@
+// kernels.cu — libnorm's sm_100a kernels for Fig. 1 `normalize` after parallel LICM
+// (the hoisted `sum` of PAPER.md:117/226-230 becomes a global
+// reduction, the kernel body `out[tid] = in[tid] / val` the scale).
+//
+// The path is HBM-bound (0.25-1 flop/B), so there is no tensor-core work: the
+// kernels are persistent grids of 256-bit vector loads (LDG.E.256) with several
+// loads in flight per thread, fp32-pairwise-then-fp64 accumulation, fixed-order
+// combines (bitwise deterministic), and PDL between the reduce and the scale.
+// DESIGN.md §4 gives each kernel's roofline and algorithmic bytes.
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+#include "norm_internal.h"
+
+namespace lnorm {
+
+// ------------------------------------------------------------------ tuning
+constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
+constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
+constexpr int FU_THREADS = 512, FU_UNROLL = 4;
+constexpr int SMALL_THREADS = 1024;
+constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 8;
+constexpr int FU_SCALE_UNROLL = 2;
+
+enum LoadKind { LD_STREAM = 0, LD_HINT = 1, LD_PLAIN = 2 };
+
+template <int K>
+__device__ __forceinline__ f8 load8(const float* p, uint64_t pol) {
+  if constexpr (K == LD_STREAM) return ld8_stream(p);
+  else if constexpr (K == LD_HINT) return ld8_policy(p, pol);
+  else return ld8(p);
+}
+
+// acc += sum of p[0, len), split over CTAs [cta, ncta) of the grid.  32-byte
+// aligned body as 8-float vectors in chunks of THREADS*UNROLL vectors (UNROLL
+// independent 256-bit loads in flight per thread); the < 8-element unaligned
+// head and < 8-element tail go to CTA 0.  The partition is a pure function of
+// (len, address mod 32, ncta), hence deterministic.
+template <int THREADS, int UNROLL, int K>
+__device__ __forceinline__ void accumulate_segment(const float* __restrict__ p, int64_t len,
+                                                   int cta, int ncta, double& acc, uint64_t pol) {
+  if (len <= 0) return;
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 31u);
+  int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
+  if (head > len) head = len;
+  const float* body = p + head;
+  const int64_t nv = (len - head) >> 3;
+  constexpr int64_t CH = (int64_t)THREADS * UNROLL;
+  const int64_t nfull = nv / CH;
+  for (int64_t c = cta; c < nfull; c += ncta) {
+    const float* q = body + (c * CH + threadIdx.x) * 8;
+    f8 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = load8<K>(q + (int64_t)u * THREADS * 8, pol);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) acc += sum8(v[u]);
+  }
+  for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
+       vi += (int64_t)ncta * THREADS)
+    acc += sum8(load8<K>(body + vi * 8, pol));
+  if (cta == 0) {
+    if ((int64_t)threadIdx.x < head) acc += (double)p[threadIdx.x];
+    const int64_t t = head + nv * 8 + threadIdx.x;
+    if (threadIdx.x < 8 && t < len) acc += (double)p[t];
+  }
+}
+
+// out[i] = in[i] / s for i in [0, len), split over CTAs; vectorised when out and
+// in are co-aligned mod 32 B (VEC), scalar otherwise.
+template <int THREADS, int UNROLL, bool VEC, bool ALIAS>
+__device__ __forceinline__ void scale_segment(float* out, const float* in, int64_t len, float s,
+                                              int cta, int ncta) {
+  if (len <= 0) return;
+  if constexpr (VEC) {
+    const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(out) & 31u);
+    int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
+    if (head > len) head = len;
+    const int64_t nv = (len - head) >> 3;
+    const float* ib = in + head;
+    float* ob = out + head;
+    constexpr int64_t CH = (int64_t)THREADS * UNROLL;
+    const int64_t nfull = nv / CH;
+    for (int64_t c = cta; c < nfull; c += ncta) {
+      const int64_t off = (c * CH + threadIdx.x) * 8;
+      f8 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        v[u] = ALIAS ? ld8(ib + off + (int64_t)u * THREADS * 8)
+                     : ld8_stream(ib + off + (int64_t)u * THREADS * 8);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], s));
+    }
+    for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
+         vi += (int64_t)ncta * THREADS) {
+      f8 v = ALIAS ? ld8(ib + vi * 8) : ld8_stream(ib + vi * 8);
+      st8_stream(ob + vi * 8, div8(v, s));
+    }
+    if (cta == 0) {
+      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], s);
+      const int64_t t = head + nv * 8 + threadIdx.x;
+      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], s);
+    }
+  } else {
+    const int64_t stride = (int64_t)ncta * THREADS;
+    for (int64_t i = (int64_t)cta * THREADS + threadIdx.x; i < len; i += stride)
+      out[i] = div_rn(in[i], s);
+  }
+}
+
+// --------------------------------------------------------------- reduce
+// Pass 1 of the two-pass path: S = sum in[0, n).  Persistent grid (2 CTAs/SM),
+// per-CTA partial, last-CTA ticket combines the partials in index order.
+__global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
+    reduce_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                  unsigned* __restrict__ ticket, double* __restrict__ S_out) {
+  // The scale kernel (PDL dependent) may be scheduled as soon as SM resources
+  // free up; it blocks in griddepcontrol.wait until this grid has completed.
+  pdl_launch_dependents();
+  __shared__ double red[RED_THREADS / 32];
+  __shared__ unsigned is_last;
+  double acc = 0.0;
+  accumulate_segment<RED_THREADS, RED_UNROLL, LD_STREAM>(in, n, blockIdx.x, gridDim.x, acc, 0);
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += RED_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    *S_out = S;
+    *ticket = 0u;  // leave the workspace reusable
+  }
+}
+
+__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full) {
+  double S = __ldcg(S_parts);
+  for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
+  *S_full = S;
+  return (float)S;  // RN to binary32
+}
+
+// ---------------------------------------------------------------- scale
+template <bool VEC, bool ALIAS>
+__global__ void __launch_bounds__(SC_THREADS)
+    scale_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
+                 int nparts, float* sum_out, double* sum_out_f64) {
+  __shared__ float s_sh;
+  pdl_wait();  // S_parts are complete and visible; `in` is no longer being read
+  if (threadIdx.x == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  __syncthreads();
+  scale_segment<SC_THREADS, SC_UNROLL, VEC, ALIAS>(out, in, len, s_sh, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(256)
+    scale_residue_kernel(float* out, const float* in, int64_t len, int64_t gbegin, int64_t G,
+                         const double* __restrict__ S_parts, int nparts, float* sum_out,
+                         double* sum_out_f64) {
+  __shared__ float s_sh;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  __syncthreads();
+  const float s = s_sh;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if ((gbegin + j) % 32 < G) out[j] = div_rn(in[j], s);  // tid = b + 32 t, b < G
+}
+
+// ---------------------------------------------------------------- small
+// One CTA does the whole call: no workspace, one launch (latency-bound sizes).
+__global__ void __launch_bounds__(SMALL_THREADS)
+    small_kernel(float* out, const float* in, int64_t n, int kind, int64_t L, int64_t G,
+                 float* sum_out, double* sum_out_f64) {
+  __shared__ double red[SMALL_THREADS / 32];
+  double acc = 0.0;
+  accumulate_segment<SMALL_THREADS, 1, LD_PLAIN>(in, n, 0, 1, acc, 0);
+  const double S = block_sum(acc, red);  // barrier: every load precedes every store
+  const float s = (float)S;
+  if (threadIdx.x == 0) {
+    if (sum_out) *sum_out = s;
+    if (sum_out_f64) *sum_out_f64 = S;
+  }
+  if (kind == COV_PREFIX) {
+    for (int64_t i = threadIdx.x; i < L; i += SMALL_THREADS) out[i] = div_rn(in[i], s);
+  } else if (kind == COV_RESIDUE) {
+    for (int64_t i = threadIdx.x; i < n; i += SMALL_THREADS)
+      if (i % 32 < G) out[i] = div_rn(in[i], s);
+  }
+}
+
+// ---------------------------------------------------------------- fused
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Single pass over HBM when the covered prefix fits in L2: the uncovered tail is
+// streamed with evict_first, the covered prefix read LAST with evict_last, grid
+// barrier, every CTA combines the partials in the same fixed order, then the
+// prefix is scaled from L2.  Co-residency guaranteed by cooperative launch.
+template <bool VEC>
+__global__ void __launch_bounds__(FU_THREADS, 2)
+    fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
+                 unsigned* bar, float* sum_out, double* sum_out_f64) {
+  __shared__ double red[FU_THREADS / 32];
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  double acc = 0.0;
+  // LD_HINT loads are coherent (no .nc): `out` may alias `in` in phase 2.
+  accumulate_segment<FU_THREADS, FU_UNROLL, LD_HINT>(in + L, n - L, blockIdx.x, gridDim.x, acc,
+                                                     pol_first);
+  accumulate_segment<FU_THREADS, FU_UNROLL, LD_HINT>(in, L, blockIdx.x, gridDim.x, acc, pol_last);
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  grid_barrier(bar);
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += FU_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);  // identical bits in every CTA
+  const float s = (float)S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sum_out) *sum_out = s;
+    if (sum_out_f64) *sum_out_f64 = S;
+  }
+  scale_segment<FU_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
+}
+
+// ----------------------------------------------------------------- rows
+__device__ __forceinline__ bool row_covered(int64_t i, int64_t L, int64_t G) {
+  return L >= 0 ? i < L : (i % 32) < G;
+}
+
+// One CTA per row (grid-strided over rows).  VEC: the row is held in registers
+// (<= ROW_THREADS*8*ROW_MAXV floats): one HBM read, block reduce, scale from
+// registers, one HBM write.  Otherwise a scalar two-sweep fallback.
+template <bool VEC, bool ALIAS, int MAXV>
+__global__ void __launch_bounds__(ROW_THREADS, 4)
+    rows_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
+  __shared__ double red[ROW_THREADS / 32];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* src = in + r * ld_in;
+    float* dst = out + r * ld_out;
+    double acc = 0.0;
+    if constexpr (VEC) {
+      const int nvr = (int)(cols >> 3);
+      f8 v[MAXV];
+#pragma unroll
+      for (int k = 0; k < MAXV; ++k) {
+        const int idx = k * ROW_THREADS + threadIdx.x;
+        if (idx < nvr) v[k] = ALIAS ? ld8(src + (int64_t)idx * 8) : ld8_stream(src + (int64_t)idx * 8);
+      }
+#pragma unroll
+      for (int k = 0; k < MAXV; ++k)
+        if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
+      const double S = block_sum(acc, red);
+      const float s = (float)S;
+      if (threadIdx.x == 0) {
+        if (sum_out) sum_out[r] = s;
+        if (sum_out_f64) sum_out_f64[r] = S;
+      }
+#pragma unroll
+      for (int k = 0; k < MAXV; ++k) {
+        const int idx = k * ROW_THREADS + threadIdx.x;
+        if (idx >= nvr) continue;
+        const int64_t e0 = (int64_t)idx * 8;
+        if (L >= 0 && e0 + 8 <= L) {
+          st8_stream(dst + e0, div8(v[k], s));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s);
+        }
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS) acc += (double)src[i];
+      const double S = block_sum(acc, red);
+      const float s = (float)S;
+      if (threadIdx.x == 0) {
+        if (sum_out) sum_out[r] = s;
+        if (sum_out_f64) sum_out_f64[r] = S;
+      }
+      for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS)
+        if (row_covered(i, L, G)) dst[i] = div_rn(src[i], s);
+    }
+  }
+}
+
+// ============================================================ launchers
+
+int reduce_grid(const DeviceInfo& d, int64_t n) {
+  const int64_t chunks = (n / 8 + (int64_t)RED_THREADS * RED_UNROLL - 1) / ((int64_t)RED_THREADS * RED_UNROLL);
+  int64_t g = (int64_t)d.sms * RED_CTAS_PER_SM;
+  if (chunks < g) g = chunks < 1 ? 1 : chunks;
+  if (g > kMaxGrid) g = kMaxGrid;
+  return (int)g;
+}
+
+cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
+                          int grid, cudaStream_t st) {
+  reduce_kernel<<<grid, RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out);
+  return cudaGetLastError();
+}
+
+template <typename Kern, typename... Args>
+static cudaError_t launch_maybe_pdl(Kern k, int grid, int block, bool pdl, cudaStream_t st,
+                                    Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
+                         int nparts, float* sum_out, double* sum_out_f64, const DeviceInfo& d,
+                         bool pdl, cudaStream_t st) {
+  const int64_t per_chunk = (int64_t)SC_THREADS * SC_UNROLL * 8;
+  int64_t g = (len + per_chunk - 1) / per_chunk;
+  const int64_t gmax = (int64_t)d.sms * SC_CTAS_PER_SM;
+  if (g > gmax) g = gmax;
+  if (g < 1) g = 1;
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
+  const bool alias = out == in;
+  if (vec && alias)
+    return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                            S_parts, nparts, sum_out, sum_out_f64);
+  if (vec)
+    return launch_maybe_pdl(scale_kernel<true, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                            S_parts, nparts, sum_out, sum_out_f64);
+  return launch_maybe_pdl(scale_kernel<false, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                          S_parts, nparts, sum_out, sum_out_f64);
+}
+
+cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64_t gbegin,
+                                 int64_t G, const double* S_parts, int nparts, float* sum_out,
+                                 double* sum_out_f64, bool pdl, cudaStream_t st) {
+  int64_t g = (len + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 1024) g = 1024;
+  return launch_maybe_pdl(scale_residue_kernel, (int)g, 256, pdl, st, out, in, len, gbegin, G,
+                          S_parts, nparts, sum_out, sum_out_f64);
+}
+
+cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,
+                         double* sum_out_f64, cudaStream_t st) {
+  small_kernel<<<1, SMALL_THREADS, 0, st>>>(out, in, cov.n, cov.kind, cov.L, cov.G, sum_out,
+                                            sum_out_f64);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,
+                         float* sum_out, double* sum_out_f64, const DeviceInfo& d,
+                         cudaStream_t st) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
+  void* fn = vec ? (void*)fused_kernel<true> : (void*)fused_kernel<false>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, FU_THREADS, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm > 2) per_sm = 2;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  int grid = d.sms * per_sm;
+  if (grid > kMaxGrid) grid = kMaxGrid;
+  int64_t n = cov.n, L = cov.L;
+  double* partials = ws.partials;
+  unsigned* bar = ws.bar;
+  void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64};
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FU_THREADS), args, 0, st);
+}
+
+cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                        int64_t ld_in, const Coverage& rc, float* sum_out, double* sum_out_f64,
+                        const DeviceInfo& d, cudaStream_t st) {
+  int64_t g = (int64_t)d.sms * ROW_CTAS_PER_SM;
+  if (rows < g) g = rows;
+  const int64_t L = rc.kind == COV_PREFIX ? rc.L : -1;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 31u) == 0 &&
+                       (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
+  const bool vec = aligned && cols <= (int64_t)ROW_THREADS * 8 * ROW_MAXV;
+  const bool alias = out == in;
+  const int maxv = cols <= ROW_THREADS * 8 ? 1 : (cols <= ROW_THREADS * 16 ? 2 : 4);
+#define NORM_ROWS(V, A, M)                                                                    \
+  rows_kernel<V, A, M><<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, \
+                                                      rc.G, sum_out, sum_out_f64)
+  if (!vec) NORM_ROWS(false, false, 1);
+  else if (alias && maxv == 1) NORM_ROWS(true, true, 1);
+  else if (alias && maxv == 2) NORM_ROWS(true, true, 2);
+  else if (alias) NORM_ROWS(true, true, 4);
+  else if (maxv == 1) NORM_ROWS(true, false, 1);
+  else if (maxv == 2) NORM_ROWS(true, false, 2);
+  else NORM_ROWS(true, false, 4);
+#undef NORM_ROWS
+  return cudaGetLastError();
+}
+
+}  // namespace lnorm

@@ -1,0 +1,507 @@
+// libnorm.cpp — the C ABI of include/libnorm.h: argument validation, the launch
+// plan (coverage of Fig. 1's grid, path choice, grid sizes), workspace
+// management, dispatch to the kernels, and the host-buffer (end-to-end) entry.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "libnorm.h"
+#include "norm_internal.h"
+
+#define NORM_API extern "C" __attribute__((visibility("default")))
+
+namespace lnorm {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& s) { g_last_error = s; }
+norm_status_t fail(norm_status_t st, const std::string& s) {
+  set_error(s);
+  return st;
+}
+norm_status_t cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return NORM_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- coverage
+// Fig. 1: normalize<<<(n+31)/32, 32>>> with tid = blockIdx.x + blockDim.x*threadIdx.x
+// (PAPER.md:103, 113).  tid = b + 32t, 0 <= b < G, 0 <= t < 32:
+//   G >= 32 -> every residue mod 32 occurs among b, tids fill [0, G+991]: C = [0, min(n, G+992))
+//   G <  32 -> tid mod 32 == b:  C = {x < n : x mod 32 < G}
+Coverage coverage_of(int64_t n, int index) {
+  Coverage c{};
+  c.n = n;
+  c.G = n > 0 ? (n + 31) / 32 : 0;
+  if (n <= 0) {
+    c.kind = COV_EMPTY;
+    return c;
+  }
+  if (index == NORM_INDEX_DENSE) {
+    c.kind = COV_PREFIX;
+    c.L = c.count = n;
+    return c;
+  }
+  if (c.G >= 32) {
+    c.kind = COV_PREFIX;
+    c.L = c.count = (n < c.G + 992) ? n : c.G + 992;
+    return c;
+  }
+  if (n <= 32) {  // G == 1: only tid 0
+    c.kind = COV_PREFIX;
+    c.L = c.count = 1;
+    return c;
+  }
+  c.kind = COV_RESIDUE;
+  const int64_t rem = n % 32;
+  c.count = (n / 32) * c.G + (rem < c.G ? rem : c.G);
+  c.L = -1;
+  return c;
+}
+
+// --------------------------------------------------------------- devices
+bool device_info(DeviceInfo* out, std::string* err) {
+  static std::mutex mu;
+  static std::vector<DeviceInfo> cache;
+  static std::vector<bool> valid;
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *err = std::string("cudaGetDevice: ") + cudaGetErrorString(e);
+    return false;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) {
+    cache.resize(dev + 1);
+    valid.resize(dev + 1, false);
+  }
+  if (!valid[dev]) {
+    DeviceInfo d{};
+    d.device = dev;
+    int l2 = 0;
+    if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+      *err = "cudaDeviceGetAttribute failed";
+      return false;
+    }
+    d.l2_bytes = (size_t)l2;
+    cache[dev] = d;
+    valid[dev] = true;
+  }
+  *out = cache[dev];
+  return true;
+}
+
+static norm_status_t check_device(DeviceInfo* d) {
+  std::string err;
+  if (!device_info(d, &err)) return fail(NORM_ERR_CUDA, err);
+  if (d->cc_major != 10 || d->cc_minor != 0)
+    return fail(NORM_ERR_UNSUPPORTED, "libnorm is built for sm_100a (B200); device is sm_" +
+                                          std::to_string(d->cc_major) + std::to_string(d->cc_minor));
+  return NORM_OK;
+}
+
+// ------------------------------------------------------------- workspace
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t workspace_bytes() {
+  return align_up(kMaxGrid * sizeof(double), 256) + 256 /* S[4] */ + 256 /* ticket, bar */;
+}
+
+Workspace workspace_carve(void* base) {
+  char* p = static_cast<char*>(base);
+  Workspace w;
+  w.partials = reinterpret_cast<double*>(p);
+  p += align_up(kMaxGrid * sizeof(double), 256);
+  w.S = reinterpret_cast<double*>(p);
+  p += 256;
+  w.ticket = reinterpret_cast<unsigned*>(p);
+  w.bar = w.ticket + 1;
+  return w;
+}
+
+// Internal cache: one zeroed workspace per (device, stream), never freed (a few KB).
+static norm_status_t internal_workspace(int dev, cudaStream_t st, Workspace* ws) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, void*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, st);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, workspace_bytes());
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error(std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+      return NORM_ERR_WORKSPACE;
+    }
+    e = cudaMemsetAsync(p, 0, workspace_bytes(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
+    it = cache.emplace(key, p).first;
+  }
+  *ws = workspace_carve(it->second);
+  return NORM_OK;
+}
+
+static norm_status_t get_workspace(const norm_opts_t* o, int dev, cudaStream_t st, Workspace* ws) {
+  if (o->workspace) {
+    if (o->workspace_bytes < workspace_bytes())
+      return fail(NORM_ERR_WORKSPACE, "workspace_bytes < norm_workspace_bytes()");
+    if (reinterpret_cast<uintptr_t>(o->workspace) & 255u)
+      return fail(NORM_ERR_INVALID_VALUE, "workspace must be 256-byte aligned");
+    *ws = workspace_carve(o->workspace);
+    return NORM_OK;
+  }
+  return internal_workspace(dev, st, ws);
+}
+
+// ------------------------------------------------------------ validation
+static bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+static norm_status_t check_opts(const norm_opts_t* o) {
+  if (o->index != NORM_INDEX_LITERAL && o->index != NORM_INDEX_DENSE)
+    return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
+  if (o->path < NORM_PATH_AUTO || o->path > NORM_PATH_SMALL)
+    return fail(NORM_ERR_INVALID_VALUE, "bad path");
+  return NORM_OK;
+}
+
+// Byte spans [a, a+na) and [b, b+nb): identical start and length -> alias (ok).
+static bool partial_overlap(const void* a, size_t na, const void* b, size_t nb) {
+  uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  if (x == y && na == nb) return false;
+  return x < y + nb && y < x + na;
+}
+
+static norm_status_t check_device_ptr(const void* p, const char* name) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaPointerGetAttributes");
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(NORM_ERR_INVALID_VALUE, std::string(name) +
+                                            " is not device memory (use norm_launch_host for host buffers)");
+  return NORM_OK;
+}
+
+static norm_status_t check_vector_args(float* out, const float* in, int64_t n) {
+  if (n < 0) return fail(NORM_ERR_INVALID_VALUE, "n < 0");
+  if (n == 0) return NORM_OK;
+  if (!out || !in) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer with n > 0");
+  if (!aligned4(out) || !aligned4(in)) return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  if (partial_overlap(out, (size_t)n * 4, in, (size_t)n * 4))
+    return fail(NORM_ERR_OVERLAP, "out and in partially overlap");
+  return NORM_OK;
+}
+
+static norm_status_t check_literal_grid(const Coverage& c, int index) {
+  if (index == NORM_INDEX_LITERAL && c.G > 2147483647LL)
+    return fail(NORM_ERR_UNSUPPORTED, "literal launch needs > 2^31-1 blocks (gridDim.x limit)");
+  return NORM_OK;
+}
+
+// AUTO path thresholds: tuned on B200.
+constexpr int64_t kSmallN = 16384;
+
+static int choose_path(const Coverage& cov, const norm_opts_t* o, const DeviceInfo& d) {
+  if (o->path != NORM_PATH_AUTO) return o->path;
+  if (cov.n <= kSmallN) return NORM_PATH_SMALL;
+  const size_t budget = d.l2_bytes / 3;  // covered bytes kept in L2 across the grid barrier
+  if (cov.kind == COV_PREFIX && (size_t)cov.L * 4 <= budget) return NORM_PATH_FUSED;
+  return NORM_PATH_TWO_PASS;
+}
+
+static norm_status_t launch_vector(float* out, const float* in, const Coverage& cov,
+                                   const norm_opts_t* o, const DeviceInfo& d) {
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  int path = choose_path(cov, o, d);
+  if (path == NORM_PATH_FUSED && cov.kind != COV_PREFIX) path = NORM_PATH_SMALL;
+  cudaError_t e;
+  if (path == NORM_PATH_SMALL) {
+    e = launch_small(out, in, cov, o->sum_out, o->sum_out_f64, st);
+    return e == cudaSuccess ? NORM_OK : cuda_fail(e, "small_kernel launch");
+  }
+  Workspace ws;
+  norm_status_t s = get_workspace(o, d.device, st, &ws);
+  if (s != NORM_OK) return s;
+  if (path == NORM_PATH_FUSED) {
+    e = launch_fused(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
+    return e == cudaSuccess ? NORM_OK : cuda_fail(e, "fused_kernel cooperative launch");
+  }
+  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  e = launch_reduce(in, cov.n, ws, ws.S, reduce_grid(d, cov.n), st);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  if (cov.kind == COV_PREFIX)
+    e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st);
+  else
+    e = launch_scale_residue(out, in, cov.n, 0, cov.G, ws.S, 1, o->sum_out, o->sum_out_f64, true, st);
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "scale_kernel launch");
+}
+
+// ----------------------------------------------------- host-buffer (e2e) path
+// Device staging per (device, stream): resident buffer for the covered elements,
+// a ring of chunk buffers for the uncovered remainder, per-chunk sums, a copy
+// stream and events.  Grows on demand, never shrinks.
+constexpr int64_t kHostChunk = 32ll << 20;  // elements per H2D chunk (128 MiB)
+constexpr int kRing = 3;
+
+struct HostStage {
+  cudaStream_t copy = nullptr;
+  float* resident = nullptr;
+  int64_t resident_cap = 0;
+  float* ring[kRing] = {};
+  double* chunkS = nullptr;
+  int64_t chunkS_cap = 0;
+  cudaEvent_t landed[2] = {};
+  cudaEvent_t slot_free[kRing] = {};
+  cudaEvent_t start = nullptr;
+  void* ws = nullptr;
+};
+
+static norm_status_t host_stage(int dev, cudaStream_t st, int64_t resident, int64_t nchunks,
+                                HostStage** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, HostStage*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  HostStage*& h = cache[std::make_pair(dev, st)];
+  cudaError_t e;
+  if (!h) {
+    h = new HostStage();
+    if ((e = cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "copy stream");
+    for (auto& ev : h->landed)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "event");
+    for (auto& ev : h->slot_free)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "event");
+    if ((e = cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "event");
+    for (auto& r : h->ring)
+      if ((e = cudaMalloc(&r, kHostChunk * 4)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(NORM_ERR_WORKSPACE, "staging ring cudaMalloc failed");
+      }
+    if ((e = cudaMalloc(&h->ws, workspace_bytes())) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NORM_ERR_WORKSPACE, "workspace cudaMalloc failed");
+    }
+    if ((e = cudaMemsetAsync(h->ws, 0, workspace_bytes(), st)) != cudaSuccess)
+      return cuda_fail(e, "workspace memset");
+  }
+  if (resident > h->resident_cap) {
+    cudaStreamSynchronize(st);  // the old buffer may still be in use
+    cudaFree(h->resident);
+    h->resident = nullptr;
+    h->resident_cap = 0;
+    if ((e = cudaMalloc(&h->resident, (size_t)resident * 4)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NORM_ERR_WORKSPACE, "resident buffer of " + std::to_string(resident * 4) +
+                                          " bytes: cudaMalloc failed");
+    }
+    h->resident_cap = resident;
+  }
+  if (nchunks > h->chunkS_cap) {
+    cudaStreamSynchronize(st);
+    cudaFree(h->chunkS);
+    h->chunkS = nullptr;
+    if ((e = cudaMalloc(&h->chunkS, (size_t)nchunks * sizeof(double))) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NORM_ERR_WORKSPACE, "chunk sums cudaMalloc failed");
+    }
+    h->chunkS_cap = nchunks;
+  }
+  *out = h;
+  return NORM_OK;
+}
+
+static norm_status_t launch_host(float* out_host, const float* in_host, const Coverage& cov,
+                                 const norm_opts_t* o, const DeviceInfo& d) {
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  const int64_t n = cov.n;
+  // Elements that must stay on the device until the divisor is known.
+  const int64_t R = cov.kind == COV_PREFIX ? cov.L : n;
+  // Chunk list: [0, R) in resident chunks, then [R, n) through the ring.
+  struct Chunk { int64_t a, b; bool res; };
+  std::vector<Chunk> chunks;
+  for (int64_t a = 0; a < R; a += kHostChunk) chunks.push_back({a, a + kHostChunk < R ? a + kHostChunk : R, true});
+  for (int64_t a = R; a < n; a += kHostChunk) chunks.push_back({a, a + kHostChunk < n ? a + kHostChunk : n, false});
+  HostStage* h = nullptr;
+  norm_status_t s = host_stage(d.device, st, R, (int64_t)chunks.size(), &h);
+  if (s != NORM_OK) return s;
+  Workspace ws = workspace_carve(h->ws);
+  cudaError_t e;
+  // Everything earlier on the caller's stream (e.g. the previous call's D2H out of
+  // the resident buffer) happens before this call's first copy.
+  if ((e = cudaEventRecord(h->start, st)) != cudaSuccess) return cuda_fail(e, "event record");
+  if ((e = cudaStreamWaitEvent(h->copy, h->start, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+  int slot = 0;
+  for (size_t k = 0; k < chunks.size(); ++k) {
+    const Chunk& c = chunks[k];
+    const int64_t len = c.b - c.a;
+    float* dst;
+    int used_slot = -1;
+    if (c.res) {
+      dst = h->resident + c.a;
+    } else {
+      used_slot = slot;
+      dst = h->ring[slot];
+      slot = (slot + 1) % kRing;
+      if ((e = cudaStreamWaitEvent(h->copy, h->slot_free[used_slot], 0)) != cudaSuccess)
+        return cuda_fail(e, "wait");
+    }
+    if ((e = cudaMemcpyAsync(dst, in_host + c.a, (size_t)len * 4, cudaMemcpyHostToDevice, h->copy)) != cudaSuccess)
+      return cuda_fail(e, "H2D copy");
+    cudaEvent_t landed = h->landed[k & 1];
+    if ((e = cudaEventRecord(landed, h->copy)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(st, landed, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    if ((e = launch_reduce(dst, len, ws, h->chunkS + k, reduce_grid(d, len), st)) != cudaSuccess)
+      return cuda_fail(e, "reduce_kernel launch");
+    if (used_slot >= 0 && (e = cudaEventRecord(h->slot_free[used_slot], st)) != cudaSuccess)
+      return cuda_fail(e, "event record");
+  }
+  const int nparts = (int)chunks.size();
+  if (cov.kind == COV_PREFIX) {
+    e = launch_scale(h->resident, h->resident, cov.L, h->chunkS, nparts, o->sum_out,
+                     o->sum_out_f64, d, false, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
+    e = cudaMemcpyAsync(out_host, h->resident, (size_t)cov.L * 4, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  } else {
+    e = launch_scale_residue(h->resident, h->resident, n, 0, cov.G, h->chunkS, nparts, o->sum_out,
+                             o->sum_out_f64, false, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scale_residue launch");
+    // covered = columns [0, G) of each 32-wide row: a strided 2-D copy
+    const int64_t full = n / 32, rem = n % 32;
+    if (full > 0) {
+      e = cudaMemcpy2DAsync(out_host, 32 * 4, h->resident, 32 * 4, (size_t)cov.G * 4, (size_t)full,
+                            cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    }
+    const int64_t last = rem < cov.G ? rem : cov.G;
+    if (last > 0) {
+      e = cudaMemcpyAsync(out_host + full * 32, h->resident + full * 32, (size_t)last * 4,
+                          cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    }
+  }
+  return NORM_OK;
+}
+
+}  // namespace lnorm
+
+using namespace lnorm;
+
+static const norm_opts_t kDefaultOpts = NORM_OPTS_INIT;
+
+// ================================================================= C ABI
+
+NORM_API norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
+  if ((s = check_vector_args(out, in, n)) != NORM_OK) return s;
+  if (n == 0) return NORM_OK;
+  const Coverage cov = coverage_of(n, o->index);
+  if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
+  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  return launch_vector(out, in, cov, o, d);
+}
+
+NORM_API norm_status_t norm_launch(float* out, const float* in, int64_t n) {
+  return norm_launch_ex(out, in, n, nullptr);
+}
+
+NORM_API norm_status_t norm_launch_host(float* out_host, const float* in_host, int64_t n,
+                                        const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
+  if ((s = check_vector_args(out_host, in_host, n)) != NORM_OK) return s;
+  if (n == 0) return NORM_OK;
+  const Coverage cov = coverage_of(n, o->index);
+  if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  return launch_host(out_host, in_host, cov, o, d);
+}
+
+NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                                 int64_t ld_out, int64_t ld_in, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
+  if (rows < 0 || cols < 0) return fail(NORM_ERR_INVALID_VALUE, "rows < 0 or cols < 0");
+  if (ld_out < cols || ld_in < cols) return fail(NORM_ERR_INVALID_VALUE, "ld < cols");
+  if (rows == 0 || cols == 0) return NORM_OK;
+  if (!out || !in) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer with work to do");
+  if (!aligned4(out) || !aligned4(in)) return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  const size_t span_out = (size_t)((rows - 1) * ld_out + cols) * 4;
+  const size_t span_in = (size_t)((rows - 1) * ld_in + cols) * 4;
+  const bool alias = out == in && ld_out == ld_in;
+  if (!alias && partial_overlap(out, span_out, in, span_in))
+    return fail(NORM_ERR_OVERLAP, "out and in rows overlap");
+  const Coverage rc = coverage_of(cols, o->index);
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
+  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  cudaError_t e = launch_rows(out, in, rows, cols, ld_out, ld_in, rc, o->sum_out, o->sum_out_f64, d,
+                              static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows_kernel launch");
+}
+
+NORM_API norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* prefix_len) {
+  if (n < 0 || !count || !prefix_len) return fail(NORM_ERR_INVALID_VALUE, "bad argument");
+  if (index != NORM_INDEX_LITERAL && index != NORM_INDEX_DENSE)
+    return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
+  const Coverage c = coverage_of(n, index);
+  *count = c.kind == COV_EMPTY ? 0 : c.count;
+  *prefix_len = c.kind == COV_EMPTY ? 0 : (c.kind == COV_PREFIX ? c.L : -1);
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_workspace_bytes(int64_t n, const norm_opts_t* o, size_t* bytes) {
+  (void)o;
+  if (n < 0 || !bytes) return fail(NORM_ERR_INVALID_VALUE, "bad argument");
+  *bytes = workspace_bytes();
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t* bytes) {
+  int64_t count, prefix;
+  norm_status_t s = norm_coverage(n, index, &count, &prefix);
+  if (s != NORM_OK) return s;
+  if (!bytes) return fail(NORM_ERR_INVALID_VALUE, "bytes is NULL");
+  *bytes = 4 * n + 8 * count;  // read all of in once + read and write C(n)
+  return NORM_OK;
+}
+
+NORM_API const char* norm_status_string(norm_status_t s) {
+  switch (s) {
+    case NORM_OK: return "NORM_OK";
+    case NORM_ERR_INVALID_VALUE: return "NORM_ERR_INVALID_VALUE";
+    case NORM_ERR_OVERLAP: return "NORM_ERR_OVERLAP";
+    case NORM_ERR_CUDA: return "NORM_ERR_CUDA";
+    case NORM_ERR_NCCL: return "NORM_ERR_NCCL";
+    case NORM_ERR_WORKSPACE: return "NORM_ERR_WORKSPACE";
+    case NORM_ERR_UNSUPPORTED: return "NORM_ERR_UNSUPPORTED";
+  }
+  return "NORM_ERR_UNKNOWN";
+}
+
+NORM_API const char* norm_last_error(void) { return g_last_error.c_str(); }

@@ -1,0 +1,87 @@
+// norm_internal.h — host-side internals of libnorm shared by the C ABI (libnorm.cpp),
+// the NCCL layer (comm.cpp) and the kernel launchers (kernels.cu).  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "libnorm.h"
+
+namespace lnorm {
+
+// Covered set C(n) of Fig. 1's launch, DESIGN.md §3.1.
+enum CovKind { COV_EMPTY = 0, COV_PREFIX = 1, COV_RESIDUE = 2 };
+struct Coverage {
+  int kind;
+  int64_t n;      // vector length
+  int64_t count;  // |C(n)|
+  int64_t L;      // COV_PREFIX: C(n) = [0, L)
+  int64_t G;      // blocks of the literal launch; COV_RESIDUE: C = {x < n : x % 32 < G}
+};
+Coverage coverage_of(int64_t n, int index);
+
+// Device workspace (one per (device, stream) in the internal cache, or carved
+// from the caller's buffer).  Must be zero-filled before first use; every
+// kernel that uses the counters returns them to zero.
+constexpr int kMaxGrid = 4096;  // max CTAs of any persistent reduce grid
+struct Workspace {
+  double* partials;  // [kMaxGrid] per-CTA partial sums
+  double* S;         // [4] fp64 sum slots (S[0]: vector sum; S[1]: sharded local partial)
+  unsigned* ticket;  // [1] last-block ticket of the reduce kernel
+  unsigned* bar;     // [2] grid barrier {count, generation} of the fused kernel
+};
+size_t workspace_bytes();
+Workspace workspace_carve(void* base);
+
+struct DeviceInfo {
+  int device;
+  int sms;
+  int cc_major, cc_minor;
+  size_t l2_bytes;
+};
+// Cached per device; returns false (with detail) if the device is unusable.
+bool device_info(DeviceInfo* out, std::string* err);
+
+// ---- kernel launchers (kernels.cu).  All return the launch's cudaError_t. ----
+// Tuning constants live next to the kernels.
+int reduce_grid(const DeviceInfo& d, int64_t n);
+
+// S_out <- sum of in[0, n) (fp64), via per-CTA partials and a last-block ticket.
+cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
+                          int grid, cudaStream_t st);
+
+// out[i] = in[i] / s for i in [0, len), s = (float)(S_parts[0] + ... + S_parts[nparts-1])
+// (fixed order).  Launched as a PDL dependent of the preceding kernel when pdl.
+// Block 0 writes sum_out / sum_out_f64 when non-null (also when len == 0).
+cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
+                         int nparts, float* sum_out, double* sum_out_f64,
+                         const DeviceInfo& d, bool pdl, cudaStream_t st);
+
+// Residue coverage (literal, G < 32): local element j is global index gbegin + j;
+// written iff (gbegin + j) % 32 < G.
+cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64_t gbegin,
+                                 int64_t G, const double* S_parts, int nparts, float* sum_out,
+                                 double* sum_out_f64, bool pdl, cudaStream_t st);
+
+// One CTA: reduce, then scale C(n).  For small n (one launch, no workspace).
+cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,
+                         double* sum_out_f64, cudaStream_t st);
+
+// One cooperative persistent kernel: reduce (covered prefix last, L2 evict_last),
+// grid barrier, scale from L2.  Requires COV_PREFIX.
+cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,
+                         float* sum_out, double* sum_out_f64, const DeviceInfo& d,
+                         cudaStream_t st);
+
+// Batched rows: one CTA per row (grid-strided), row held in registers when it fits.
+cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                        int64_t ld_in, const Coverage& row_cov, float* sum_out,
+                        double* sum_out_f64, const DeviceInfo& d, cudaStream_t st);
+
+// thread-local error detail
+void set_error(const std::string& s);
+norm_status_t fail(norm_status_t st, const std::string& s);
+norm_status_t cuda_fail(cudaError_t e, const char* what);
+
+}  // namespace lnorm

@@ -1,0 +1,320 @@
+"""GPU parity: libnorm's CUDA path (through the C ABI) vs the CPU oracle.
+
+For every case: |s - S| <= 1e-6 |S| (Σ|x| for signed inputs), per-element
+relative error <= 1e-5 against the oracle, bitwise replay out[i] == in[i] ⊘ s
+over the whole array (which also proves every uncovered element still holds its
+sentinel), and bitwise-identical results over repeated runs (R15).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+import paper_2207_00257_b200 as L
+
+pytestmark = pytest.mark.gpu
+
+SENTINEL_BITS = 0x7FC0FFEE  # a quiet NaN payload no kernel produces
+PATHS = ["auto", "two_pass", "fused", "small"]
+DISTS = [0, 1, 2, 3, 4]
+
+
+def sentinel(n):
+    return np.full(n, SENTINEL_BITS, dtype=np.uint32).view(np.float32)
+
+
+def to_dev(x):
+    return torch.from_numpy(x).cuda()
+
+
+def run(x_host, mode, path, out_init=None, in_place=False):
+    n = x_host.size
+    inp = to_dev(x_host)
+    out = inp if in_place else to_dev(sentinel(n) if out_init is None else out_init)
+    s = torch.zeros(1, dtype=torch.float32, device="cuda")
+    S = torch.zeros(1, dtype=torch.float64, device="cuda")
+    L.normalize(out, inp, index=mode, path=path, sum_out=s, sum_out_f64=S)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), np.float32(s.item()), S.item()
+
+
+def check(x, out, s, mode, dist_kind, before=None):
+    n = x.size
+    S = oracle.sum_exact(x)
+    scale = oracle.sum_abs_exact(x) if dist_kind == 3 else abs(S)
+    assert abs(float(s) - S) <= 1e-6 * scale, (float(s), S)
+    before = sentinel(n) if before is None else before
+    rep = oracle.replay(x, s, mode, out=before.copy())
+    assert out.view(np.uint32).tobytes() == rep.view(np.uint32).tobytes(), "replay mismatch"
+    ref = oracle.normalize(x, mode, out=before.copy())
+    cov = oracle.covered_mask(n, mode)
+    r, o = ref[cov].astype(np.float64), out[cov].astype(np.float64)
+    nz = r != 0
+    if dist_kind != 3:  # signed: ill-conditioned quotient, replay above is the check
+        assert np.all(np.abs(o[nz] - r[nz]) <= 1e-5 * np.abs(r[nz]))
+        assert np.all(o[~nz] == 0)
+
+
+SIZES = [1, 7, 8, 31, 32, 33, 100, 992, 993, 1024, 1025, 1026, 4099, 16384, 16385,
+         2**20 - 1, 2**20 + 7, 3 * 2**20 + 5]
+
+
+def test_generator_device_matches_host():
+    for d in DISTS:
+        for n, off in [(1000003, 0), (4099, 2**31 + 5)]:
+            h = gen.make_host(n, seed=2207, dist=d, offset=off)
+            t = torch.empty(n, dtype=torch.float32, device="cuda")
+            gen.fill_cuda(t, seed=2207, dist=d, offset=off)
+            assert t.cpu().numpy().tobytes() == h.tobytes()
+
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+@pytest.mark.parametrize("path", PATHS)
+def test_parity_sizes(mode, path):
+    for i, n in enumerate(SIZES):
+        if path == "small" and n > 2**20:
+            continue
+        d = DISTS[i % len(DISTS)]
+        x = gen.make_host(n, seed=i, dist=d)
+        out, s, S = run(x, mode, path)
+        check(x, out, s, mode, d)
+        assert np.float32(S) == s
+
+
+@pytest.mark.parametrize("dist_kind", DISTS)
+@pytest.mark.parametrize("seed", [0, 1, 2207])
+def test_parity_distributions(dist_kind, seed):
+    n = 2**20 + 7
+    x = gen.make_host(n, seed=seed, dist=dist_kind)
+    for mode in ("literal", "dense"):
+        for path in ("two_pass", "fused"):
+            out, s, _ = run(x, mode, path)
+            check(x, out, s, mode, dist_kind)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_deterministic_repeat(path):
+    x = gen.make_host(3 * 2**20 + 5 if path != "small" else 50000, seed=9, dist=4)
+    outs = [run(x, "dense", path) for _ in range(3)]
+    for o, s, S in outs[1:]:
+        assert o.tobytes() == outs[0][0].tobytes() and s == outs[0][1] and S == outs[0][2]
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_alignment_offsets(path):
+    n = 2**18 + 3
+    for off_in in (0, 1, 3, 7):
+        for off_out in (0, 1, 3, 7):
+            x = gen.make_host(n, seed=off_in * 8 + off_out, dist=0)
+            buf_in = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+            buf_out = torch.from_numpy(np.concatenate([sentinel(8), sentinel(n)])).cuda()
+            inp = buf_in[off_in:off_in + n]
+            inp.copy_(torch.from_numpy(x))
+            out = buf_out[off_out:off_out + n]
+            s = torch.zeros(1, device="cuda")
+            L.normalize(out, inp, index="literal", path=path, sum_out=s)
+            torch.cuda.synchronize()
+            check(x, out.cpu().numpy(), np.float32(s.item()), "literal", 0)
+            full = buf_out.cpu().numpy()
+            assert np.all(full[:off_out].view(np.uint32) == SENTINEL_BITS)
+            assert np.all(full[off_out + n:].view(np.uint32) == SENTINEL_BITS)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_in_place(path, mode):
+    for n in (1000, 2**20 + 7):
+        if path == "small" and n > 2**20:
+            continue
+        x = gen.make_host(n, seed=n, dist=4)
+        out, s, _ = run(x, mode, path, in_place=True)
+        check(x, out, s, mode, 4, before=x)  # uncovered elements keep the input bits
+
+
+def test_special_values():
+    cases = {
+        "zeros": np.zeros(5000, np.float32),
+        "one_inf": np.concatenate([np.ones(4000, np.float32), [np.inf]]).astype(np.float32),
+        "both_inf": np.array([np.inf, -np.inf] + [1.0] * 3000, np.float32),
+        "nan": np.array([1.0] * 3000 + [np.nan], np.float32),
+        "subnormal": np.full(4096, 1e-45, np.float32),
+        "neg_zero": np.full(100, -0.0, np.float32),
+        "cancel": np.concatenate([np.full(2048, 1.0), np.full(2048, -1.0), [2.0**-20]]).astype(np.float32),
+    }
+    for name, x in cases.items():
+        for path in ("two_pass", "fused", "small"):
+            out, s, _ = run(x, "dense", path)
+            S = oracle.sum_exact(x)
+            if math.isnan(S):
+                assert math.isnan(s), name
+            elif math.isinf(S):
+                assert s == S, name
+            else:
+                assert abs(float(s) - S) <= 1e-6 * max(abs(S), oracle.sum_abs_exact(x) * 1e-30), name
+            rep = oracle.replay(x, s, "dense", out=sentinel(x.size))
+            same = (out.view(np.uint32) == rep.view(np.uint32)) | (np.isnan(out) & np.isnan(rep))
+            assert same.all(), name
+
+
+def test_large_sampled_2_28():
+    n = 2**28
+    for mode in ("literal", "dense"):
+        inp = torch.empty(n, dtype=torch.float32, device="cuda")
+        gen.fill_cuda(inp, seed=1, dist=0)
+        for path in ("two_pass", "fused") if mode == "literal" else ("two_pass",):
+            out = torch.full((n,), 0.0, device="cuda").view(torch.int32).fill_(SENTINEL_BITS).view(torch.float32)
+            s = torch.zeros(1, device="cuda")
+            L.normalize(out, inp, index=mode, path=path, sum_out=s)
+            torch.cuda.synchronize()
+            x = inp.cpu().numpy()
+            S = oracle.sum_exact(x)
+            sv = np.float32(s.item())
+            assert abs(float(sv) - S) <= 1e-6 * S
+            count, prefix = oracle.coverage_closed(n, mode)
+            o = out.cpu().numpy()
+            k = min(prefix, 1 << 24)
+            assert np.array_equal(o[:k], x[:k] / sv)  # bitwise replay of the covered prefix (sample)
+            rng = np.random.default_rng(0)
+            idx = rng.integers(0, n, 200000)
+            cov = idx < prefix
+            assert np.array_equal(o[idx[cov]], x[idx[cov]] / sv)
+            assert np.all(o[idx[~cov]].view(np.uint32) == SENTINEL_BITS)
+            ref = (x[idx[cov]].astype(np.float64) / S)
+            assert np.all(np.abs(o[idx[cov]] - ref) <= 1e-5 * ref)
+        del inp
+
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_rows_parity(mode):
+    shapes = [(65536, 4096, 4096), (7, 1000, 1000), (3, 4099, 4100), (5, 10000, 10000),
+              (33, 64, 72), (4, 700, 703), (1, 8192, 8192), (2, 1, 1)]
+    for i, (R, C, ld) in enumerate(shapes):
+        d = DISTS[i % 5]
+        x = np.zeros((R, ld), np.float32)
+        x[:, :C] = gen.make_host(R * C, seed=i, dist=d).reshape(R, C)
+        inp = to_dev(x)
+        out = to_dev(sentinel(R * ld).reshape(R, ld))
+        s = torch.zeros(R, device="cuda")
+        L.normalize_rows(out[:, :C], inp[:, :C], index=mode, sum_out=s)
+        torch.cuda.synchronize()
+        o, sv = out.cpu().numpy(), s.cpu().numpy()
+        rows_to_check = range(R) if R <= 64 else np.random.default_rng(i).integers(0, R, 64)
+        for r in rows_to_check:
+            check(x[r, :C], o[r, :C], sv[r], mode, d)
+        assert np.all(o[:, C:].view(np.uint32) == SENTINEL_BITS)
+        if R > 64:  # full-size config: replay every row with its own divisor
+            cov = oracle.covered_mask(C, mode)
+            q = x[:, :C][:, cov] / sv[:, None]
+            assert np.array_equal(o[:, :C][:, cov], q)
+            assert np.all(o[:, :C][:, ~cov].view(np.uint32) == SENTINEL_BITS)
+
+
+def test_rows_deterministic_and_in_place():
+    R, C = 1000, 4096
+    x = gen.make_host(R * C, seed=5, dist=4).reshape(R, C)
+    a = to_dev(x)
+    o1 = torch.empty_like(a)
+    o2 = torch.empty_like(a)
+    L.normalize_rows(o1, a, index="dense")
+    L.normalize_rows(o2, a, index="dense")
+    b = a.clone()
+    L.normalize_rows(b, b, index="dense")
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(o1, b)
+
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_host_entry(mode):
+    for n in (100, 2**20 + 7, (32 << 20) * 2 + 12345):
+        x = torch.from_numpy(gen.make_host(n, seed=n % 97, dist=0)).pin_memory()
+        out = torch.from_numpy(sentinel(n)).pin_memory()
+        s = torch.zeros(1, device="cuda")
+        L.normalize_host(out, x, index=mode, sum_out=s)
+        torch.cuda.synchronize()
+        check(x.numpy(), out.numpy(), np.float32(s.item()), mode, 0)
+
+
+def test_sharded_world1():
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = L.Comm()
+        for mode in ("literal", "dense"):
+            for n in (700, 2**20 + 7):
+                x = gen.make_host(n, seed=4, dist=0)
+                ranges = L.plan_shards(n, 1, mode)[0]
+                inp = to_dev(x)
+                out = to_dev(sentinel(n))
+                s = torch.zeros(1, device="cuda")
+                comm.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s)
+                torch.cuda.synchronize()
+                check(x, out.cpu().numpy(), np.float32(s.item()), mode, 0)
+        comm.destroy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_user_workspace_matches_internal():
+    n = 3 * 2**20 + 5
+    x = gen.make_host(n, seed=3, dist=4)
+    inp = to_dev(x)
+    ws = torch.zeros(L.workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    a, b = torch.empty_like(inp), torch.empty_like(inp)
+    L.normalize(a, inp, index="dense", path="two_pass")
+    L.normalize(b, inp, index="dense", path="two_pass", workspace=ws)
+    L.normalize(b, inp, index="dense", path="two_pass", workspace=ws)  # reusable
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_cuda_graph_capture():
+    n = 2**22 + 3
+    inp = to_dev(gen.make_host(n, seed=1, dist=0))
+    ref = torch.empty_like(inp)
+    out = torch.empty_like(inp)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        L.normalize(ref, inp, index="dense", path="two_pass")  # warm-up allocates the workspace
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            L.normalize(out, inp, index="dense", path="two_pass")
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+
+
+def test_host_pointer_rejected():
+    x = torch.ones(100)
+    import ctypes
+    st = L.lib().norm_launch(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(x.data_ptr()), 100)
+    assert st == L._lib.STATUS.index("NORM_ERR_INVALID_VALUE")
+
+
+@pytest.mark.slow
+def test_full_size_2_32_sampled():
+    """BASELINE configs[3] at W = 1, the launch bench.py times: literal two-pass."""
+    n = 2**32
+    inp = torch.empty(n, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(inp, seed=2207, dist=0)
+    out = torch.empty(n, dtype=torch.int32, device="cuda").fill_(SENTINEL_BITS).view(torch.float32)
+    s = torch.zeros(1, device="cuda")
+    L.normalize(out, inp, index="literal", sum_out=s)
+    torch.cuda.synchronize()
+    sv = np.float32(s.item())
+    x = inp.cpu().numpy()
+    S = oracle.sum_exact(x)
+    assert abs(float(sv) - S) <= 1e-6 * S
+    count, L_ = oracle.coverage_closed(n)
+    o = out[:L_].cpu().numpy()
+    assert np.array_equal(o, x[:L_] / sv)  # every covered element, bitwise replay
+    ref = x[:L_].astype(np.float64) / S
+    assert np.max(np.abs(o - ref) / ref) <= 1e-5
+    rng = np.random.default_rng(1)
+    idx = torch.from_numpy(rng.integers(L_, n, 1 << 20)).cuda()
+    assert torch.all(out.view(torch.int32)[idx] == SENTINEL_BITS)
