@@ -110,6 +110,9 @@ def _opts(index, path, stream, sum_out, sum_out_f64, workspace=None, events=None
         o.workspace = workspace.data_ptr()
         o.workspace_bytes = workspace.numel() * workspace.element_size()
     if events is not None:
+        for ev in events:  # torch creates the CUDA event lazily, on first record
+            if not ev.cuda_event:
+                ev.record()
         o.ev_reduce_begin = events[0].cuda_event
         o.ev_reduce_end = events[1].cuda_event
     return o

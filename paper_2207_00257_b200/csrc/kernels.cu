@@ -19,7 +19,7 @@ constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
 constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
 constexpr int FU_THREADS = 512, FU_UNROLL = 4;
 constexpr int SMALL_THREADS = 1024;
-constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 8;
+constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 4;
 constexpr int FU_SCALE_UNROLL = 2;
 
 enum LoadKind { LD_STREAM = 0, LD_HINT = 1, LD_PLAIN = 2 };
@@ -261,59 +261,92 @@ __device__ __forceinline__ bool row_covered(int64_t i, int64_t L, int64_t G) {
   return L >= 0 ? i < L : (i % 32) < G;
 }
 
-// One CTA per row (grid-strided over rows).  VEC: the row is held in registers
-// (<= ROW_THREADS*8*ROW_MAXV floats): one HBM read, block reduce, scale from
-// registers, one HBM write.  Otherwise a scalar two-sweep fallback.
-template <bool VEC, bool ALIAS, int MAXV>
-__global__ void __launch_bounds__(ROW_THREADS, 4)
-    rows_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
-                int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
+// Batched rows, register-resident (row <= ROW_THREADS*8*MAXV floats, 32 B aligned,
+// cols % 8 == 0): persistent CTAs walk rows r, r + grid, ...; the NEXT row's
+// 256-bit loads are issued before the current row's block reduction, so HBM
+// always has a row in flight per CTA (software pipelining across rows).  One
+// HBM read and one write (of the covered part) per element.
+template <bool ALIAS, int MAXV>
+__device__ __forceinline__ void row_load(const float* src, int nvr, f8* v) {
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int idx = k * ROW_THREADS + threadIdx.x;
+    if (idx < nvr) v[k] = ALIAS ? ld8(src + (int64_t)idx * 8) : ld8_stream(src + (int64_t)idx * 8);
+  }
+}
+
+template <int MAXV>
+__device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int64_t r, int64_t L,
+                                           int64_t G, double* red, float* sum_out,
+                                           double* sum_out_f64) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k)
+    if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
+  const double S = block_sum(acc, red);
+  const float s = (float)S;
+  if (threadIdx.x == 0) {
+    if (sum_out) sum_out[r] = s;
+    if (sum_out_f64) sum_out_f64[r] = S;
+  }
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int idx = k * ROW_THREADS + threadIdx.x;
+    if (idx >= nvr) continue;
+    const int64_t e0 = (int64_t)idx * 8;
+    if (L >= 0 && e0 + 8 <= L) {
+      st8_stream(dst + e0, div8(v[k], s));
+    } else if (L < 0 || e0 < L) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s);
+    }
+  }
+}
+
+__host__ __device__ constexpr int row_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : ROW_CTAS_PER_SM; }
+
+template <bool ALIAS, int MAXV>
+__global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
+    rows_vec_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                    int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
+  __shared__ double red[ROW_THREADS / 32];
+  const int nvr = (int)(cols >> 3);
+  const int64_t step = gridDim.x;
+  f8 a[MAXV], b[MAXV];
+  int64_t r = blockIdx.x;
+  if (r < rows) row_load<ALIAS, MAXV>(in + r * ld_in, nvr, a);
+  while (r < rows) {
+    int64_t rn = r + step;
+    if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, b);
+    row_finish<MAXV>(out + r * ld_out, nvr, a, r, L, G, red, sum_out, sum_out_f64);
+    r = rn;
+    if (r >= rows) break;
+    rn = r + step;
+    if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, a);
+    row_finish<MAXV>(out + r * ld_out, nvr, b, r, L, G, red, sum_out, sum_out_f64);
+    r = rn;
+  }
+}
+
+// Any shape / alignment: one CTA per row, a scalar sum sweep then a scale sweep.
+__global__ void __launch_bounds__(ROW_THREADS)
+    rows_generic_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                        int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
   __shared__ double red[ROW_THREADS / 32];
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const float* src = in + r * ld_in;
     float* dst = out + r * ld_out;
     double acc = 0.0;
-    if constexpr (VEC) {
-      const int nvr = (int)(cols >> 3);
-      f8 v[MAXV];
-#pragma unroll
-      for (int k = 0; k < MAXV; ++k) {
-        const int idx = k * ROW_THREADS + threadIdx.x;
-        if (idx < nvr) v[k] = ALIAS ? ld8(src + (int64_t)idx * 8) : ld8_stream(src + (int64_t)idx * 8);
-      }
-#pragma unroll
-      for (int k = 0; k < MAXV; ++k)
-        if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
-      const double S = block_sum(acc, red);
-      const float s = (float)S;
-      if (threadIdx.x == 0) {
-        if (sum_out) sum_out[r] = s;
-        if (sum_out_f64) sum_out_f64[r] = S;
-      }
-#pragma unroll
-      for (int k = 0; k < MAXV; ++k) {
-        const int idx = k * ROW_THREADS + threadIdx.x;
-        if (idx >= nvr) continue;
-        const int64_t e0 = (int64_t)idx * 8;
-        if (L >= 0 && e0 + 8 <= L) {
-          st8_stream(dst + e0, div8(v[k], s));
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s);
-        }
-      }
-    } else {
-      for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS) acc += (double)src[i];
-      const double S = block_sum(acc, red);
-      const float s = (float)S;
-      if (threadIdx.x == 0) {
-        if (sum_out) sum_out[r] = s;
-        if (sum_out_f64) sum_out_f64[r] = S;
-      }
-      for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS)
-        if (row_covered(i, L, G)) dst[i] = div_rn(src[i], s);
+    for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS) acc += (double)src[i];
+    const double S = block_sum(acc, red);  // barrier: the row's loads precede its stores
+    const float s = (float)S;
+    if (threadIdx.x == 0) {
+      if (sum_out) sum_out[r] = s;
+      if (sum_out_f64) sum_out_f64[r] = S;
     }
+    for (int64_t i = threadIdx.x; i < cols; i += ROW_THREADS)
+      if (row_covered(i, L, G)) dst[i] = div_rn(src[i], s);
   }
 }
 
@@ -408,24 +441,26 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
 cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                         int64_t ld_in, const Coverage& rc, float* sum_out, double* sum_out_f64,
                         const DeviceInfo& d, cudaStream_t st) {
-  int64_t g = (int64_t)d.sms * ROW_CTAS_PER_SM;
+  const int maxv = cols <= ROW_THREADS * 8 ? 1 : (cols <= ROW_THREADS * 16 ? 2 : 4);
+  int64_t g = (int64_t)d.sms * row_ctas_per_sm(maxv);  // persistent: one wave
   if (rows < g) g = rows;
   const int64_t L = rc.kind == COV_PREFIX ? rc.L : -1;
   const bool aligned = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 31u) == 0 &&
                        (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
   const bool vec = aligned && cols <= (int64_t)ROW_THREADS * 8 * ROW_MAXV;
   const bool alias = out == in;
-  const int maxv = cols <= ROW_THREADS * 8 ? 1 : (cols <= ROW_THREADS * 16 ? 2 : 4);
-#define NORM_ROWS(V, A, M)                                                                    \
-  rows_kernel<V, A, M><<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, \
-                                                      rc.G, sum_out, sum_out_f64)
-  if (!vec) NORM_ROWS(false, false, 1);
-  else if (alias && maxv == 1) NORM_ROWS(true, true, 1);
-  else if (alias && maxv == 2) NORM_ROWS(true, true, 2);
-  else if (alias) NORM_ROWS(true, true, 4);
-  else if (maxv == 1) NORM_ROWS(true, false, 1);
-  else if (maxv == 2) NORM_ROWS(true, false, 2);
-  else NORM_ROWS(true, false, 4);
+#define NORM_ROWS(A, M)                                                                           \
+  rows_vec_kernel<A, M><<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, rc.G, \
+                                                       sum_out, sum_out_f64)
+  if (!vec)
+    rows_generic_kernel<<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, rc.G,
+                                                        sum_out, sum_out_f64);
+  else if (alias && maxv == 1) NORM_ROWS(true, 1);
+  else if (alias && maxv == 2) NORM_ROWS(true, 2);
+  else if (alias) NORM_ROWS(true, 4);
+  else if (maxv == 1) NORM_ROWS(false, 1);
+  else if (maxv == 2) NORM_ROWS(false, 2);
+  else NORM_ROWS(false, 4);
 #undef NORM_ROWS
   return cudaGetLastError();
 }
