@@ -475,13 +475,55 @@ def run_paths28(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_licm(args, world, rank, local):
+    """Fig. 1 before/after parallel LICM on the GPU — the
+    printed per-thread O(N^2) kernel, the per-block O(N^2/B) variant and the
+    hoisted O(N) path, timed at small n."""
+    import torch
+    import gen
+    import paper_2207_00257_b200 as L
+    stream = torch.cuda.current_stream()
+    res = []
+    for e in (10, 12, 14, 16, 18):
+        n = 2**e
+        inp = torch.empty(n, dtype=torch.float32, device="cuda")
+        gen.fill_cuda(inp, seed=2207, dist="unit")
+        out = torch.empty_like(inp)
+        row = {"n": n}
+        for form in ("per_thread", "per_block", "hoisted"):
+            if form == "per_thread" and e > 16:
+                continue
+            for _ in range(2):
+                L.normalize_form(out, inp, form=form, index=args.index)
+            reps = 5 if form != "hoisted" else 50
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                L.normalize_form(out, inp, form=form, index=args.index)
+            b.record(stream)
+            torch.cuda.synchronize()
+            row[form + "_ms"] = a.elapsed_time(b) / reps
+        if "per_thread_ms" in row:
+            row["per_thread_over_hoisted"] = row["per_thread_ms"] / row["hoisted_ms"]
+        row["per_block_over_hoisted"] = row["per_block_ms"] / row["hoisted_ms"]
+        res.append(row)
+    last = res[-1]
+    line = {"metric": "Fig. 1 before/after parallel LICM on B200 (ms per call)",
+            "value": last["per_block_over_hoisted"], "unit": "x (per-block / hoisted, n=2^18)",
+            "n_gpus": 1, "steps": 5, "warmup": 2, "higher_is_better": True, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "config": {"workload": f"normalize_form, {args.index} index"},
+            "forms": res, "gpu_launches": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="libnorm", choices=["libnorm", "reference"])
-    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28"])
+    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
     ap.add_argument("--n", type=int, default=2**32)
@@ -501,6 +543,8 @@ def main():
             run_vector(args, world, rank, local)
         elif args.workload == "rows":
             run_rows(args, world, rank, local)
+        elif args.workload == "licm":
+            run_licm(args, world, rank, local)
         else:
             run_paths28(args, world, rank, local)
     finally:

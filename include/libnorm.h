@@ -121,6 +121,23 @@ norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, const norm_
 norm_status_t norm_launch_host(float* out_host, const float* in_host, int64_t n,
                                const norm_opts_t* o);
 
+/* ------------------------------------------------ before LICM (NEXT-1) */
+
+typedef enum {
+  NORM_FORM_HOISTED = 0,    /* after parallel LICM: one O(N) sum (== norm_launch_ex)      */
+  NORM_FORM_PER_BLOCK = 1,  /* thread 0 of each block sums, O(N^2/B)    */
+  NORM_FORM_PER_THREAD = 2  /* PAPER.md:108, as printed: every thread sums, O(N^2)        */
+} norm_form_t;
+
+/* Fig. 1 in the given form, for timing the LICM before/after on the GPU
+ * (PAPER.md:117, 226-228).  The un-hoisted forms run the printed launch
+ * normalize<<<(n+31)/32, 32>>> with the index of o->index and a sequential fp64
+ * `sum` in every summing thread; o->path is ignored for them.  out == in is
+ * rejected for the un-hoisted forms (they race as printed; reading R9), and
+ * n > 2^24 is rejected for them (NORM_ERR_UNSUPPORTED: O(N^2) work). */
+norm_status_t norm_launch_form(float* out, const float* in, int64_t n, int32_t form,
+                               const norm_opts_t* o);
+
 /* ------------------------------------------------------------------ rows */
 
 /* Batched per-row variant (reading R10; BASELINE configs[4]): for each row r,

@@ -18,6 +18,8 @@ from ._lib import (  # noqa: F401
     last_error,
     lib,
     normalize,
+    normalize_form,
+    FORM,
     normalize_host,
     normalize_rows,
     plan_shards,
@@ -28,7 +30,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_rows", "normalize_host", "coverage", "algorithmic_bytes",
+    "normalize", "normalize_form", "FORM", "normalize_rows", "normalize_host", "coverage", "algorithmic_bytes",
     "plan_shards", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

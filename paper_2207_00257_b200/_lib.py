@@ -49,6 +49,7 @@ def lib():
             "norm_launch": [vp, vp, i64],
             "norm_launch_ex": [vp, vp, i64, optp],
             "norm_launch_host": [vp, vp, i64, optp],
+            "norm_launch_form": [vp, vp, i64, i32, optp],
             "norm_rows": [vp, vp, i64, i64, i64, i64, optp],
             "norm_coverage": [i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "norm_workspace_bytes": [i64, optp, ctypes.POINTER(ctypes.c_size_t)],
@@ -140,6 +141,23 @@ def normalize(out, inp, index="literal", path="auto", stream=None, sum_out=None,
         raise ValueError("out and inp must be contiguous with equal numel")
     o = _opts(index, path, stream, sum_out, sum_out_f64, workspace, events, inp.device)
     _check(lib().norm_launch_ex(out.data_ptr(), inp.data_ptr(), inp.numel(), ctypes.byref(o)))
+    return out
+
+
+FORM = {"hoisted": 0, "per_block": 1, "per_thread": 2}
+
+
+def normalize_form(out, inp, form="hoisted", index="literal", stream=None, sum_out=None,
+                   sum_out_f64=None):
+    """Fig. 1 before / after parallel LICM (norm_launch_form): "per_thread" (as
+    printed, O(N^2)), "per_block" (shared-memory comment, O(N^2/B)) or "hoisted"."""
+    _check_f32(out, "out")
+    _check_f32(inp, "inp")
+    if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
+        raise ValueError("out and inp must be contiguous with equal numel")
+    o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=inp.device)
+    _check(lib().norm_launch_form(out.data_ptr(), inp.data_ptr(), inp.numel(), _enum(FORM, form),
+                                  ctypes.byref(o)))
     return out
 
 

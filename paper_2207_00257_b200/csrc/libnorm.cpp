@@ -426,6 +426,27 @@ NORM_API norm_status_t norm_launch(float* out, const float* in, int64_t n) {
   return norm_launch_ex(out, in, n, nullptr);
 }
 
+NORM_API norm_status_t norm_launch_form(float* out, const float* in, int64_t n, int32_t form,
+                                        const norm_opts_t* o) {
+  if (form == NORM_FORM_HOISTED) return norm_launch_ex(out, in, n, o);
+  if (!o) o = &kDefaultOpts;
+  if (form != NORM_FORM_PER_BLOCK && form != NORM_FORM_PER_THREAD)
+    return fail(NORM_ERR_INVALID_VALUE, "bad form");
+  norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
+  if ((s = check_vector_args(out, in, n)) != NORM_OK) return s;
+  if (n == 0) return NORM_OK;
+  if (out == in) return fail(NORM_ERR_OVERLAP, "un-hoisted forms race under aliasing (reading R9)");
+  if (n > (1ll << 24)) return fail(NORM_ERR_UNSUPPORTED, "un-hoisted forms are O(N^2): n <= 2^24");
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
+  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  cudaError_t e = launch_unhoisted(out, in, n, o->index, form, o->sum_out, o->sum_out_f64,
+                                   static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "unhoisted kernel launch");
+}
+
 NORM_API norm_status_t norm_launch_host(float* out_host, const float* in_host, int64_t n,
                                         const norm_opts_t* o) {
   if (!o) o = &kDefaultOpts;

@@ -79,6 +79,11 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
                         int64_t ld_in, const Coverage& row_cov, float* sum_out,
                         double* sum_out_f64, const DeviceInfo& d, cudaStream_t st);
 
+// Fig. 1 before LICM (unhoisted.cu): the printed launch <<<(n+31)/32, 32>>> with
+// `sum` per thread (NORM_FORM_PER_THREAD) or per block (NORM_FORM_PER_BLOCK).
+cudaError_t launch_unhoisted(float* out, const float* in, int64_t n, int index, int form,
+                             float* sum_out, double* sum_out_f64, cudaStream_t st);
+
 // thread-local error detail
 void set_error(const std::string& s);
 norm_status_t fail(norm_status_t st, const std::string& s);

@@ -318,3 +318,77 @@ def test_full_size_2_32_sampled():
     rng = np.random.default_rng(1)
     idx = torch.from_numpy(rng.integers(L_, n, 1 << 20)).cuda()
     assert torch.all(out.view(torch.int32)[idx] == SENTINEL_BITS)
+
+
+# ------------------------------------------------- before LICM (NEXT-1) forms
+
+@pytest.mark.parametrize("form", ["per_thread", "per_block", "hoisted"])
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_unhoisted_forms_parity(form, mode):
+    for i, n in enumerate([1, 33, 100, 1024, 1025, 4099, 2**16 + 3]):
+        d = DISTS[i % 5]
+        x = gen.make_host(n, seed=100 + i, dist=d)
+        inp = to_dev(x)
+        out = to_dev(sentinel(n))
+        s = torch.zeros(1, device="cuda")
+        L.normalize_form(out, inp, form=form, index=mode, sum_out=s)
+        torch.cuda.synchronize()
+        check(x, out.cpu().numpy(), np.float32(s.item()), mode, d)
+        # the oracle's own form gives the same covered set and the same values within 1e-5
+        ref, _ = {"per_thread": oracle.form_thread, "per_block": oracle.form_block,
+                  "hoisted": oracle.form_hoisted}[form](x, mode, sentinel(n))
+        o = out.cpu().numpy()
+        assert np.array_equal(np.isnan(o) & (o.view(np.uint32) == SENTINEL_BITS),
+                              ref.view(np.uint32) == SENTINEL_BITS)
+
+
+def test_unhoisted_forms_agree_and_reject():
+    n = 5000
+    x = gen.make_host(n, seed=1, dist=0)
+    inp = to_dev(x)
+    outs = []
+    for form in ("per_thread", "per_block"):
+        out = torch.empty_like(inp)
+        s = torch.zeros(1, device="cuda")
+        L.normalize_form(out, inp, form=form, index="dense", sum_out=s)
+        torch.cuda.synchronize()
+        outs.append((out.cpu().numpy(), s.item()))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes() and outs[0][1] == outs[1][1]
+    with pytest.raises(L.NormError):
+        L.normalize_form(inp, inp, form="per_thread")
+    big = torch.empty(2**24 + 1, device="cuda")
+    with pytest.raises(L.NormError):
+        L.normalize_form(big, big.clone(), form="per_block")
+
+
+def test_sharded_multirange_local_semantics():
+    """World-1 NCCL comm driven with another rank's two-range shard: exercises the
+    range -> local-offset mapping and the per-range covered sub-ranges of
+    norm_launch_sharded.  With W = 1 the divisor is the sum of the local elements."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29534"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = L.Comm()
+        for n, W, k, mode in [(2**20 + 7, 4, 1, "literal"), (2**20 + 7, 4, 3, "literal"),
+                              (700, 3, 1, "literal"), (3 * 2**20 + 5, 8, 5, "dense")]:
+            ranges = L.plan_shards(n, W, mode, True)[k]
+            x = np.concatenate([gen.make_host(ln, seed=7, dist=0, offset=b) for b, ln in ranges])
+            inp = to_dev(x)
+            out = to_dev(sentinel(x.size))
+            s = torch.zeros(1, device="cuda")
+            comm.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s)
+            torch.cuda.synchronize()
+            sv = np.float32(s.item())
+            S = oracle.sum_exact(x)
+            assert abs(float(sv) - S) <= 1e-6 * S
+            gidx = np.concatenate([np.arange(b, b + ln) for b, ln in ranges])
+            cov = oracle.covered_mask(n, mode)[gidx]
+            o = out.cpu().numpy()
+            assert np.array_equal(o[cov], x[cov] / sv)
+            assert np.all(o[~cov].view(np.uint32) == SENTINEL_BITS)
+        comm.destroy()
+    finally:
+        dist.destroy_process_group()
