@@ -44,6 +44,12 @@ def lib():
             getattr(L, f).argtypes = [vp, vp, i64, ctypes.c_int, u64p]
         L.oracle_rows.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
         L.oracle_replay.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float]
+        L.oracle_softmax_rows.argtypes = [vp, vp, i64, i64, i64, i64]
+        L.oracle_log_softmax_rows.argtypes = [vp, vp, i64, i64, i64, i64]
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.oracle_nll_forward.argtypes = [vp, dp, vp, vp, vp, i64, i64, i64, ctypes.c_int, i64]
+        L.oracle_nll_backward.argtypes = [vp, vp, vp, vp, ctypes.c_double, i64, i64, i64,
+                                          ctypes.c_int, i64]
         _lib = L
     return _lib
 
@@ -149,3 +155,48 @@ def replay(inp, s, mode="literal", out=None):
         out = np.zeros_like(inp)
     assert lib().oracle_replay(out.ctypes.data, pin, inp.size, _mode(mode), float(s)) == 0
     return out
+
+
+# ------------------------------------------------ NEXT-2: softmax and ClassNLL
+
+RED = {"none": 0, "mean": 1, "sum": 2}
+
+
+def softmax_rows(x2d, log=False):
+    """Row softmax (or log-softmax) in fp64, rounded once to fp32."""
+    x2d = np.ascontiguousarray(x2d, dtype=np.float32)
+    R, C = x2d.shape
+    out = np.zeros_like(x2d)
+    f = lib().oracle_log_softmax_rows if log else lib().oracle_softmax_rows
+    assert f(out.ctypes.data, x2d.ctypes.data, R, C, C, C) == 0
+    return out
+
+
+def nll_forward(logp, target, weight=None, reduction="mean", ignore_index=-100):
+    """ClassNLLCriterion_updateOutput (PAPER.md:747-750) in fp64: (loss, total_weight)."""
+    logp = np.ascontiguousarray(logp, dtype=np.float32)
+    target = np.ascontiguousarray(target, dtype=np.int64)
+    N, C = logp.shape
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+    loss = np.zeros(max(N, 1) if reduction == "none" else 1, dtype=np.float64)
+    tw = ctypes.c_double()
+    rc = lib().oracle_nll_forward(loss.ctypes.data, ctypes.byref(tw), logp.ctypes.data,
+                                  target.ctypes.data, None if w is None else w.ctypes.data,
+                                  N, C, C, RED[reduction], ignore_index)
+    assert rc == 0
+    return (loss[:N] if reduction == "none" else loss[0]), tw.value
+
+
+def nll_backward(grad_out, target, C, weight=None, reduction="mean", ignore_index=-100,
+                 total_weight=1.0):
+    """ClassNLLCriterion_updateGradInput in fp64: dense [N, C] gradient."""
+    target = np.ascontiguousarray(target, dtype=np.int64)
+    N = target.size
+    g = np.ascontiguousarray(np.atleast_1d(grad_out), dtype=np.float64)
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+    grad = np.zeros((N, C), dtype=np.float64)
+    rc = lib().oracle_nll_backward(grad.ctypes.data, g.ctypes.data, target.ctypes.data,
+                                   None if w is None else w.ctypes.data, float(total_weight),
+                                   N, C, C, RED[reduction], ignore_index)
+    assert rc == 0
+    return grad

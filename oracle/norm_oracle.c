@@ -248,3 +248,97 @@ int oracle_replay(float* out, const float* in, int64_t n, int mode, float s) {
     if (oracle_is_covered(n, mode, i)) out[i] = in[i] / s; /* binary32 RN */
   return 0;
 }
+
+/* ================================================================ NEXT-2
+ * Row softmax / log-softmax and ClassNLLCriterion (the PyTorch
+ * CUDA kernels MocCUDA transpiles: "aggregation operations like Softmax" and the
+ * NLL loss that uses __syncthreads).  Textbook definitions in fp64. */
+
+static int rowop_args(int64_t rows, int64_t cols, int64_t ld_out, int64_t ld_in, const void* a,
+                      const void* b) {
+  if (rows < 0 || cols < 0 || ld_out < cols || ld_in < cols) return 1;
+  if (rows > 0 && cols > 0 && (!a || !b)) return 1;
+  return 0;
+}
+
+/* max over the row; NaN if any element is NaN (IEEE maximum propagating NaN). */
+static double row_max(const float* x, int64_t cols) {
+  double m = -INFINITY;
+  for (int64_t i = 0; i < cols; ++i) {
+    if (isnan(x[i])) return NAN;
+    if ((double)x[i] > m) m = (double)x[i];
+  }
+  return m;
+}
+
+int oracle_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                        int64_t ld_in) {
+  if (rowop_args(rows, cols, ld_out, ld_in, out, in)) return 1;
+  for (int64_t r = 0; r < rows; ++r) {
+    const float* x = in + r * ld_in;
+    float* y = out + r * ld_out;
+    const double m = row_max(x, cols);
+    double S = 0.0;
+    for (int64_t i = 0; i < cols; ++i) S += exp((double)x[i] - m);
+    for (int64_t i = 0; i < cols; ++i) y[i] = (float)(exp((double)x[i] - m) / S);
+  }
+  return 0;
+}
+
+int oracle_log_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                            int64_t ld_out, int64_t ld_in) {
+  if (rowop_args(rows, cols, ld_out, ld_in, out, in)) return 1;
+  for (int64_t r = 0; r < rows; ++r) {
+    const float* x = in + r * ld_in;
+    float* y = out + r * ld_out;
+    const double m = row_max(x, cols);
+    double S = 0.0;
+    for (int64_t i = 0; i < cols; ++i) S += exp((double)x[i] - m);
+    const double lse = log(S);
+    for (int64_t i = 0; i < cols; ++i) y[i] = (float)(((double)x[i] - m) - lse);
+  }
+  return 0;
+}
+
+int oracle_nll_forward(double* loss, double* total_weight, const float* logp, const int64_t* target,
+                       const float* weight, int64_t N, int64_t C, int64_t ld, int reduction,
+                       int64_t ignore_index) {
+  if (N < 0 || C < 1 || ld < C || !loss || !total_weight || (N > 0 && (!logp || !target))) return 1;
+  if (reduction < ORACLE_RED_NONE || reduction > ORACLE_RED_SUM) return 1;
+  double num = 0.0, den = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    const int64_t t = target[i];
+    double li;
+    if (t == ignore_index) {
+      li = 0.0;
+    } else if (t < 0 || t >= C) {
+      li = NAN;
+    } else {
+      const double w = weight ? (double)weight[t] : 1.0;
+      li = -w * (double)logp[i * ld + t];
+      den += w;
+    }
+    if (reduction == ORACLE_RED_NONE) loss[i] = li;
+    num += li;
+  }
+  *total_weight = den;
+  if (reduction == ORACLE_RED_SUM) loss[0] = num;
+  if (reduction == ORACLE_RED_MEAN) loss[0] = num / den; /* 0/0 -> NaN when all ignored */
+  return 0;
+}
+
+int oracle_nll_backward(double* grad, const double* grad_out, const int64_t* target,
+                        const float* weight, double total_weight, int64_t N, int64_t C, int64_t ld,
+                        int reduction, int64_t ignore_index) {
+  if (N < 0 || C < 1 || ld < C || (N > 0 && (!grad || !grad_out || !target))) return 1;
+  if (reduction < ORACLE_RED_NONE || reduction > ORACLE_RED_SUM) return 1;
+  for (int64_t i = 0; i < N; ++i) {
+    for (int64_t c = 0; c < C; ++c) grad[i * ld + c] = 0.0;
+    const int64_t t = target[i];
+    if (t == ignore_index || t < 0 || t >= C) continue;
+    const double w = weight ? (double)weight[t] : 1.0;
+    const double g = grad_out[reduction == ORACLE_RED_NONE ? i : 0];
+    grad[i * ld + t] = -w * g / (reduction == ORACLE_RED_MEAN ? total_weight : 1.0);
+  }
+  return 0;
+}

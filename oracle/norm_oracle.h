@@ -65,6 +65,32 @@ int oracle_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t
 /* Replay given a divisor s: out[i] = in[i] / s in binary32 RN for i in C(n). */
 int oracle_replay(float* out, const float* in, int64_t n, int mode, float s);
 
+/* ---- the PyTorch kernels the paper transpiles next to
+ * normalize — "aggregation operations like Softmax" and ClassNLLCriterion
+ * (PAPER.md:747-750).  fp64 throughout; parity pins in tests/test_oracle_rowops.py. */
+
+/* Row softmax: out = exp(x - max) / sum exp(x - max), fp64, then rounded once. */
+int oracle_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                        int64_t ld_in);
+/* Row log-softmax: out = (x - max) - log(sum exp(x - max)). */
+int oracle_log_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                            int64_t ld_out, int64_t ld_in);
+
+enum { ORACLE_RED_NONE = 0, ORACLE_RED_MEAN = 1, ORACLE_RED_SUM = 2 };
+/* ClassNLLCriterion_updateOutput: per sample i with t = target[i] != ignore_index,
+ * l_i = -w[t] * logp[i*ld + t] (w = 1 without weights).  NONE: loss[i] = l_i (0 if
+ * ignored); SUM: loss[0] = sum l_i; MEAN: loss[0] = sum l_i / sum w[t_i] (NaN if
+ * the weight sum is 0).  *total_weight = sum w[t_i].  A target outside [0, C) that
+ * is not ignore_index gives NaN (reading R17). */
+int oracle_nll_forward(double* loss, double* total_weight, const float* logp, const int64_t* target,
+                       const float* weight, int64_t N, int64_t C, int64_t ld, int reduction,
+                       int64_t ignore_index);
+/* ClassNLLCriterion_updateGradInput: grad[i*ld + c] = 0 except
+ * grad[i*ld + t_i] = -w[t_i] * g_i / (MEAN ? total_weight : 1), g_i = grad_out[NONE ? i : 0]. */
+int oracle_nll_backward(double* grad, const double* grad_out, const int64_t* target,
+                        const float* weight, double total_weight, int64_t N, int64_t C, int64_t ld,
+                        int reduction, int64_t ignore_index);
+
 #ifdef __cplusplus
 }
 #endif

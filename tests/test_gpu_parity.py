@@ -318,6 +318,32 @@ def test_full_size_2_32_sampled():
     rng = np.random.default_rng(1)
     idx = torch.from_numpy(rng.integers(L_, n, 1 << 20)).cuda()
     assert torch.all(out.view(torch.int32)[idx] == SENTINEL_BITS)
+    # dense index on the same input (bench's dense_index figure): every element covered
+    s2 = torch.zeros(1, device="cuda")
+    L.normalize(out, inp, index="dense", sum_out=s2)
+    torch.cuda.synchronize()
+    sv2 = np.float32(s2.item())
+    assert abs(float(sv2) - S) <= 1e-6 * S
+    head = out[: 1 << 24].cpu().numpy()
+    assert np.array_equal(head, x[: 1 << 24] / sv2)
+    sidx = rng.integers(0, n, 1 << 22)
+    o = out[torch.from_numpy(sidx).cuda()].cpu().numpy()
+    assert np.array_equal(o, x[sidx] / sv2)
+    tail = out[n - 4099:].cpu().numpy()
+    assert np.array_equal(tail, x[n - 4099:] / sv2)
+
+
+def test_empty_and_degenerate():
+    e = torch.empty(0, device="cuda")
+    L.normalize(e, e)
+    L.normalize(e, e, index="dense", path="two_pass")
+    L.normalize_rows(torch.empty(0, 5, device="cuda"), torch.empty(0, 5, device="cuda"))
+    L.normalize_rows(torch.empty(3, 0, device="cuda"), torch.empty(3, 0, device="cuda"))
+    one = torch.tensor([4.0], device="cuda")
+    o = torch.zeros(1, device="cuda")
+    L.normalize(o, one)
+    torch.cuda.synchronize()
+    assert o.item() == 1.0
 
 
 # ------------------------------------------------- before LICM (NEXT-1) forms
@@ -392,3 +418,27 @@ def test_sharded_multirange_local_semantics():
         comm.destroy()
     finally:
         dist.destroy_process_group()
+
+
+def test_torch_ops():
+    import paper_2207_00257_b200.torch_ops as T
+    x = to_dev(gen.make_host(3 * 2**20 + 5, seed=3, dist=0))
+    y = torch.ops.libnorm.normalize(x, "dense")
+    ref = torch.empty_like(x)
+    L.normalize(ref, x, index="dense")
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    assert torch.allclose(y, (x.double() / x.double().sum()).float(), rtol=1e-5, atol=0)
+    z = torch.ops.libnorm.normalize(x, "literal")  # uncovered elements keep x
+    c, p = L.coverage(x.numel())
+    assert torch.equal(z[p:], x[p:]) and torch.equal(z[:p], ref[:p] * 0 + z[:p])
+    m = to_dev(gen.make_host(64 * 4096, seed=4, dist=0).reshape(64, 4096))
+    r = T.Normalize("dense")(m)
+    assert torch.allclose(r, (m.double() / m.double().sum(-1, keepdim=True)).float(), rtol=1e-5, atol=0)
+    w = m.clone()
+    torch.ops.libnorm.normalize_(w, "dense")
+    assert torch.allclose(w.sum(), torch.tensor(1.0, device="cuda"), rtol=1e-5)
+    f = torch.compile(lambda t: torch.ops.libnorm.normalize_rows(t * 2.0, "dense"), fullgraph=True)
+    assert torch.allclose(f(m), r, rtol=1e-6, atol=0)
+    with pytest.raises(RuntimeError):
+        torch.ops.libnorm.normalize(torch.ones(4), "dense")
