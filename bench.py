@@ -475,6 +475,86 @@ def run_paths28(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_softmax(args, world, rank, local):
+    """row softmax over the rows config (65536 x 4096 fp32)."""
+    import torch
+    import gen
+    import paper_2207_00257_b200 as L
+    R, C = 65536, 4096
+    inp = torch.empty(R * C, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(inp, seed=2207, dist="signed")
+    inp = inp.view(R, C)
+    out = torch.empty_like(inp)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    res = {}
+    peak, src = load_peak()
+    for log in (False, True):
+        for _ in range(args.warmup):
+            L.softmax_rows(out, inp, log=log)
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            L.softmax_rows(out, inp, log=log)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = sum(times) / len(times)
+        v = 8 * R * C / (ms / 1e3) / 1e9
+        res["log_softmax" if log else "softmax"] = {"ms_per_step": ms, "value": v, "frac": v / peak}
+        # torch's own kernel on the same data, for context
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            y = (torch.log_softmax if log else torch.softmax)(inp, dim=1)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        tms = sum(times) / len(times)
+        res[("log_softmax" if log else "softmax") + "_torch"] = {"ms_per_step": tms,
+                                                                 "value": 8 * R * C / (tms / 1e3) / 1e9}
+    # ClassNLLCriterion on the same shape (log-probs = log_softmax output)
+    L.softmax_rows(out, inp, log=True)
+    tgt = torch.empty(R, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(tgt, seed=5, dist="unit")
+    tgt = (tgt * C).long()
+    grad = torch.empty_like(out)
+    g1 = torch.ones(1, device="cuda")
+    for _ in range(args.warmup):
+        loss, tw = L.nll_forward(out, tgt)
+        L.nll_backward(g1, (R, C), tgt, tw, grad=grad)
+    for name in ("nll_forward", "nll_backward"):
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            if name == "nll_forward":
+                loss, tw = L.nll_forward(out, tgt)
+            else:
+                L.nll_backward(g1, (R, C), tgt, tw, grad=grad)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = sum(times) / len(times)
+        nbytes = R * (8 + 4) if name == "nll_forward" else 4 * R * C  # gathered reads / dense write
+        res[name] = {"ms_per_step": ms, "value": nbytes / (ms / 1e3) / 1e9, "bytes": nbytes}
+    line = {"metric": "row softmax GB/s and % of HBM peak (65536x4096 fp32)",
+            "value": res["softmax"]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["softmax"]["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "norm_softmax_rows 65536x4096 fp32 (D3 signed logits)",
+                       "l2": "flushed (256 MiB write) before every step"},
+            "frac_of_hbm_peak": res["softmax"]["frac"], "peak": peak, "results": res,
+            "gpu_launches": args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_licm(args, world, rank, local):
     """Fig. 1 before/after parallel LICM on the GPU — the
     printed per-thread O(N^2) kernel, the per-block O(N^2/B) variant and the
@@ -523,7 +603,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="libnorm", choices=["libnorm", "reference"])
-    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm"])
+    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
     ap.add_argument("--n", type=int, default=2**32)
@@ -543,6 +623,8 @@ def main():
             run_vector(args, world, rank, local)
         elif args.workload == "rows":
             run_rows(args, world, rank, local)
+        elif args.workload == "softmax":
+            run_softmax(args, world, rank, local)
         elif args.workload == "licm":
             run_licm(args, world, rank, local)
         else:

@@ -147,6 +147,43 @@ norm_status_t norm_launch_form(float* out, const float* in, int64_t n, int32_t f
 norm_status_t norm_rows(float* out, const float* in, int64_t rows, int64_t cols,
                         int64_t ld_out, int64_t ld_in, const norm_opts_t* o);
 
+/* ------------------------------------------- row ops (NEXT-2) */
+/* The PyTorch CUDA kernels the paper transpiles beside normalize: "aggregation
+ * operations like Softmax" and ClassNLLCriterion.  Same
+ * conventions as above; o->stream / o->workspace are used, the other opts fields
+ * are ignored.  Tolerances: DESIGN.md §9. */
+
+typedef enum { NORM_SOFTMAX = 0, NORM_LOG_SOFTMAX = 1 } norm_softmax_t;
+
+/* out[r, i] = exp(x - m_r) / sum_j exp(x_j - m_r)  (softmax), or
+ * (x - m_r) - log(sum_j exp(x_j - m_r))             (log-softmax), m_r = max of row r.
+ * A row containing NaN gives NaN; rows are [rows][ld], ld >= cols; out == in with
+ * equal ld is allowed (in place); partial overlap -> NORM_ERR_OVERLAP. */
+norm_status_t norm_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                                int64_t ld_out, int64_t ld_in, int32_t kind,
+                                const norm_opts_t* o);
+
+typedef enum { NORM_REDUCTION_NONE = 0, NORM_REDUCTION_MEAN = 1, NORM_REDUCTION_SUM = 2 } norm_reduction_t;
+
+/* ClassNLLCriterion_updateOutput.  logp: [N][ld] log-probabilities, target: int64[N],
+ * weight: optional fp32[C] (NULL = 1).  Sample i with t = target[i] != ignore_index
+ * contributes l_i = -w[t] * logp[i, t]; a target outside [0, C) that is not
+ * ignore_index contributes NaN (reading R17).  NONE: loss[i] = l_i (0 if ignored),
+ * loss is fp32[N]; SUM / MEAN: loss[0] = sum l_i (/ sum w[t_i]).  total_weight
+ * (optional, fp32[1]) = sum w[t_i].  Deterministic (fixed-order fp64 reduction). */
+norm_status_t norm_nll_forward(float* loss, float* total_weight, const float* logp,
+                               const int64_t* target, const float* weight, int64_t N, int64_t C,
+                               int64_t ld, int32_t reduction, int64_t ignore_index,
+                               const norm_opts_t* o);
+
+/* ClassNLLCriterion_updateGradInput: writes the whole [N][ld] grad (cols [0, C)):
+ * zeros except grad[i, t_i] = -w[t_i] * g_i / (MEAN ? *total_weight : 1), with
+ * g_i = grad_out[NONE ? i : 0].  total_weight (device fp32[1]) is required for MEAN. */
+norm_status_t norm_nll_backward(float* grad, const float* grad_out, const int64_t* target,
+                                const float* weight, const float* total_weight, int64_t N,
+                                int64_t C, int64_t ld, int32_t reduction, int64_t ignore_index,
+                                const norm_opts_t* o);
+
 /* ------------------------------------------------------------ host-only */
 
 /* Size of C(n) for the index mode; *prefix_len = L if C(n) == [0, L), else -1.

@@ -22,6 +22,10 @@ from ._lib import (  # noqa: F401
     FORM,
     normalize_host,
     normalize_rows,
+    softmax_rows,
+    nll_forward,
+    nll_backward,
+    REDUCTION,
     plan_shards,
     status_string,
     workspace_bytes,
@@ -30,7 +34,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "FORM", "normalize_rows", "normalize_host", "coverage", "algorithmic_bytes",
+    "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
     "plan_shards", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

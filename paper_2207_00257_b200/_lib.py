@@ -50,6 +50,9 @@ def lib():
             "norm_launch_ex": [vp, vp, i64, optp],
             "norm_launch_host": [vp, vp, i64, optp],
             "norm_launch_form": [vp, vp, i64, i32, optp],
+            "norm_softmax_rows": [vp, vp, i64, i64, i64, i64, i32, optp],
+            "norm_nll_forward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
+            "norm_nll_backward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
             "norm_rows": [vp, vp, i64, i64, i64, i64, optp],
             "norm_coverage": [i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "norm_workspace_bytes": [i64, optp, ctypes.POINTER(ctypes.c_size_t)],
@@ -159,6 +162,56 @@ def normalize_form(out, inp, form="hoisted", index="literal", stream=None, sum_o
     _check(lib().norm_launch_form(out.data_ptr(), inp.data_ptr(), inp.numel(), _enum(FORM, form),
                                   ctypes.byref(o)))
     return out
+
+
+REDUCTION = {"none": 0, "mean": 1, "sum": 2}
+
+
+def softmax_rows(out, inp, log=False, stream=None):
+    """Row softmax / log-softmax of 2-D float32 CUDA tensors (norm_softmax_rows)."""
+    _check_f32(out, "out")
+    _check_f32(inp, "inp")
+    if out.dim() != 2 or out.shape != inp.shape:
+        raise ValueError("out and inp must be 2-D with equal shapes")
+    if out.shape[1] > 1 and (out.stride(1) != 1 or inp.stride(1) != 1):
+        raise ValueError("rows must have unit column stride")
+    o = _opts("literal", "auto", stream, None, None, device=inp.device)
+    _check(lib().norm_softmax_rows(out.data_ptr(), inp.data_ptr(), inp.shape[0], inp.shape[1],
+                                   out.stride(0), inp.stride(0), 1 if log else 0, ctypes.byref(o)))
+    return out
+
+
+def nll_forward(logp, target, weight=None, reduction="mean", ignore_index=-100, stream=None):
+    """ClassNLLCriterion_updateOutput: returns (loss, total_weight) CUDA tensors."""
+    import torch
+    _check_f32(logp, "logp")
+    if logp.dim() != 2 or (logp.shape[1] > 1 and logp.stride(1) != 1):
+        raise ValueError("logp must be 2-D with unit column stride")
+    if target.dtype != torch.int64 or not target.is_cuda or not target.is_contiguous():
+        raise ValueError("target must be a contiguous int64 CUDA tensor")
+    N, C = logp.shape
+    red = _enum(REDUCTION, reduction)
+    loss = torch.empty(N if red == 0 else 1, dtype=torch.float32, device=logp.device)
+    tw = torch.empty(1, dtype=torch.float32, device=logp.device)
+    o = _opts("literal", "auto", stream, None, None, device=logp.device)
+    _check(lib().norm_nll_forward(loss.data_ptr(), tw.data_ptr(), logp.data_ptr(), target.data_ptr(),
+                                  _ptr(weight), N, C, logp.stride(0), red, ignore_index,
+                                  ctypes.byref(o)))
+    return (loss if red == 0 else loss[0]), tw
+
+
+def nll_backward(grad_out, logp_shape, target, total_weight, weight=None, reduction="mean",
+                 ignore_index=-100, grad=None, stream=None):
+    """ClassNLLCriterion_updateGradInput: returns the dense [N, C] float32 gradient."""
+    import torch
+    N, C = logp_shape
+    if grad is None:
+        grad = torch.empty((N, C), dtype=torch.float32, device=target.device)
+    o = _opts("literal", "auto", stream, None, None, device=target.device)
+    _check(lib().norm_nll_backward(grad.data_ptr(), grad_out.data_ptr(), target.data_ptr(),
+                                   _ptr(weight), _ptr(total_weight), N, C, grad.stride(0),
+                                   _enum(REDUCTION, reduction), ignore_index, ctypes.byref(o)))
+    return grad
 
 
 def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):

@@ -486,6 +486,74 @@ NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int6
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows_kernel launch");
 }
 
+NORM_API norm_status_t norm_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                                         int64_t ld_out, int64_t ld_in, int32_t kind,
+                                         const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  if (kind != NORM_SOFTMAX && kind != NORM_LOG_SOFTMAX) return fail(NORM_ERR_INVALID_VALUE, "bad kind");
+  if (rows < 0 || cols < 0) return fail(NORM_ERR_INVALID_VALUE, "rows < 0 or cols < 0");
+  if (ld_out < cols || ld_in < cols) return fail(NORM_ERR_INVALID_VALUE, "ld < cols");
+  if (rows == 0 || cols == 0) return NORM_OK;
+  if (!out || !in) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer with work to do");
+  if (!aligned4(out) || !aligned4(in)) return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  const size_t span_out = (size_t)((rows - 1) * ld_out + cols) * 4;
+  const size_t span_in = (size_t)((rows - 1) * ld_in + cols) * 4;
+  if (!(out == in && ld_out == ld_in) && partial_overlap(out, span_out, in, span_in))
+    return fail(NORM_ERR_OVERLAP, "out and in rows overlap");
+  norm_status_t s;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
+  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  cudaError_t e = launch_softmax_rows(out, in, rows, cols, ld_out, ld_in, kind == NORM_LOG_SOFTMAX, d,
+                                      static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "softmax kernel launch");
+}
+
+static norm_status_t check_nll(int64_t N, int64_t C, int64_t ld, int32_t reduction) {
+  if (N < 0 || C < 1 || ld < C) return fail(NORM_ERR_INVALID_VALUE, "need N >= 0, C >= 1, ld >= C");
+  if (reduction < NORM_REDUCTION_NONE || reduction > NORM_REDUCTION_SUM)
+    return fail(NORM_ERR_INVALID_VALUE, "bad reduction");
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_nll_forward(float* loss, float* total_weight, const float* logp,
+                                        const int64_t* target, const float* weight, int64_t N,
+                                        int64_t C, int64_t ld, int32_t reduction,
+                                        int64_t ignore_index, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_nll(N, C, ld, reduction)) != NORM_OK) return s;
+  if (!loss || (N > 0 && (!logp || !target))) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
+  if (reduction == NORM_REDUCTION_NONE && N == 0) return NORM_OK;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Workspace ws;
+  if ((s = get_workspace(o, d.device, st, &ws)) != NORM_OK) return s;
+  cudaError_t e = launch_nll_forward(loss, total_weight, logp, target, weight, N, C, ld, reduction,
+                                     ignore_index, ws, d, st);
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "nll_forward launch");
+}
+
+NORM_API norm_status_t norm_nll_backward(float* grad, const float* grad_out, const int64_t* target,
+                                         const float* weight, const float* total_weight, int64_t N,
+                                         int64_t C, int64_t ld, int32_t reduction,
+                                         int64_t ignore_index, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_nll(N, C, ld, reduction)) != NORM_OK) return s;
+  if (N == 0) return NORM_OK;
+  if (!grad || !grad_out || !target) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
+  if (reduction == NORM_REDUCTION_MEAN && !total_weight)
+    return fail(NORM_ERR_INVALID_VALUE, "MEAN needs total_weight");
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  cudaError_t e = launch_nll_backward(grad, grad_out, target, weight, total_weight, N, C, ld,
+                                      reduction, ignore_index, d, static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "nll_backward launch");
+}
+
 NORM_API norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* prefix_len) {
   if (n < 0 || !count || !prefix_len) return fail(NORM_ERR_INVALID_VALUE, "bad argument");
   if (index != NORM_INDEX_LITERAL && index != NORM_INDEX_DENSE)

@@ -84,6 +84,19 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
 cudaError_t launch_unhoisted(float* out, const float* in, int64_t n, int index, int form,
                              float* sum_out, double* sum_out_f64, cudaStream_t st);
 
+// NEXT-2 row ops (rowops.cu)
+cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                                int64_t ld_out, int64_t ld_in, bool log, const DeviceInfo& d,
+                                cudaStream_t st);
+cudaError_t launch_nll_forward(float* loss, float* total_weight, const float* logp,
+                               const int64_t* target, const float* weight, int64_t N, int64_t C,
+                               int64_t ld, int reduction, int64_t ignore_index,
+                               const Workspace& ws, const DeviceInfo& d, cudaStream_t st);
+cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_t* target,
+                                const float* weight, const float* total_weight, int64_t N,
+                                int64_t C, int64_t ld, int reduction, int64_t ignore_index,
+                                const DeviceInfo& d, cudaStream_t st);
+
 // thread-local error detail
 void set_error(const std::string& s);
 norm_status_t fail(norm_status_t st, const std::string& s);

@@ -1,0 +1,317 @@
+// rowops.cu — SURVEY §8(f) NEXT-2: the reduce->elementwise PyTorch kernels the
+// paper transpiles next to `normalize`: row Softmax /
+// LogSoftmax ("aggregation operations like Softmax") and ClassNLLCriterion
+// updateOutput / updateGradInput (the NLL loss "uses CUDA's __syncthreads()").
+//
+// Softmax reuses the rows skeleton of kernels.cu: one row per CTA held in
+// registers (256-bit loads), the next row prefetched before the current row's
+// reductions, block max -> exp -> fp64 block sum -> scale, one HBM read and one
+// write per element.  NLL forward is a gather + deterministic two-level
+// reduction (per-CTA partials, last-CTA ticket); NLL backward is a write stream
+// (zeros plus one value per row).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "device_common.cuh"
+#include "norm_internal.h"
+
+namespace lnorm {
+
+constexpr int SM_THREADS = 256;
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block max (exact, order-independent); NaN propagation is handled by the caller.
+__device__ __forceinline__ float block_max(float v, float* redf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) redf[warp] = v;
+  __syncthreads();
+  float t = lane < nw ? redf[lane] : -INFINITY;
+  return warp_max(t);
+}
+
+// exp(d) for d = x - m <= 0 as 2^(d * log2 e) on the SFU (MUFU.EX2).  Relative
+// error <= |d|·2^-24 (rounding of d, then of d·log2 e) + 2^-22 (ex2.approx):
+// below 5.1e-6 for |d| <= 80; smaller results are below 1.8e-35.
+__device__ __forceinline__ float exp_shifted(float d) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(d * 1.4426950408889634f));
+  return y;
+}
+
+template <int MAXV>
+__device__ __forceinline__ void sm_load(const float* src, int nvr, f8* v) {
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int idx = k * SM_THREADS + threadIdx.x;
+    if (idx < nvr) v[k] = ld8_stream(src + (int64_t)idx * 8);
+  }
+}
+
+// softmax / log-softmax of one register-resident row.
+template <bool LOG, int MAXV>
+__device__ __forceinline__ void sm_finish(float* dst, int nvr, f8* v, float* redf, double* redd) {
+  float m = -INFINITY;
+  int nan = 0;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k)
+    if (k * SM_THREADS + (int)threadIdx.x < nvr)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        m = fmaxf(m, v[k].v[j]);
+        nan |= isnan(v[k].v[j]);
+      }
+  m = block_max(m, redf);
+  if (__syncthreads_or(nan)) m = __int_as_float(0x7fffffff);  // NaN row -> NaN everywhere
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k)
+    if (k * SM_THREADS + (int)threadIdx.x < nvr) {
+      f8 e;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) e.v[j] = exp_shifted(v[k].v[j] - m);
+      acc += sum8(e);
+      if (!LOG) v[k] = e;
+    }
+  const double S = block_sum(acc, redd);
+  if (LOG) {
+    const float lse = (float)log(S);
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int idx = k * SM_THREADS + threadIdx.x;
+      if (idx < nvr) {
+        f8 y;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y.v[j] = (v[k].v[j] - m) - lse;
+        st8_stream(dst + (int64_t)idx * 8, y);
+      }
+    }
+  } else {
+    // y = e * (1/S): one rounding of 1/S and one of the product (< 1.2e-7 relative)
+    const float rs = (float)(1.0 / S);
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int idx = k * SM_THREADS + threadIdx.x;
+      if (idx < nvr) {
+        f8 y;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y.v[j] = v[k].v[j] * rs;
+        st8_stream(dst + (int64_t)idx * 8, y);
+      }
+    }
+  }
+}
+
+__host__ __device__ constexpr int sm_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : 4; }
+
+template <bool LOG, int MAXV>
+__global__ void __launch_bounds__(SM_THREADS, sm_ctas_per_sm(MAXV))
+    softmax_vec_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                       int64_t ld_in) {
+  __shared__ float redf[SM_THREADS / 32];
+  __shared__ double redd[SM_THREADS / 32];
+  const int nvr = (int)(cols >> 3);
+  const int64_t step = gridDim.x;
+  f8 a[MAXV], b[MAXV];
+  int64_t r = blockIdx.x;
+  if (r < rows) sm_load<MAXV>(in + r * ld_in, nvr, a);
+  while (r < rows) {
+    int64_t rn = r + step;
+    if (rn < rows) sm_load<MAXV>(in + rn * ld_in, nvr, b);
+    sm_finish<LOG, MAXV>(out + r * ld_out, nvr, a, redf, redd);
+    r = rn;
+    if (r >= rows) break;
+    rn = r + step;
+    if (rn < rows) sm_load<MAXV>(in + rn * ld_in, nvr, a);
+    sm_finish<LOG, MAXV>(out + r * ld_out, nvr, b, redf, redd);
+    r = rn;
+  }
+}
+
+// Any shape / alignment / in-place: three sweeps over the row from memory.
+template <bool LOG>
+__global__ void __launch_bounds__(SM_THREADS)
+    softmax_generic_kernel(float* out, const float* in, int64_t rows, int64_t cols,
+                           int64_t ld_out, int64_t ld_in) {
+  __shared__ float redf[SM_THREADS / 32];
+  __shared__ double redd[SM_THREADS / 32];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* x = in + r * ld_in;
+    float* y = out + r * ld_out;
+    float m = -INFINITY;
+    int nan = 0;
+    for (int64_t i = threadIdx.x; i < cols; i += SM_THREADS) {
+      const float xi = x[i];
+      m = fmaxf(m, xi);
+      nan |= isnan(xi);
+    }
+    m = block_max(m, redf);
+    if (__syncthreads_or(nan)) m = __int_as_float(0x7fffffff);
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < cols; i += SM_THREADS) acc += (double)exp_shifted(x[i] - m);
+    const double S = block_sum(acc, redd);  // barrier: every read precedes every write
+    const float rs = (float)(1.0 / S), lse = (float)log(S);
+    for (int64_t i = threadIdx.x; i < cols; i += SM_THREADS) {
+      const float d = x[i] - m;
+      y[i] = LOG ? d - lse : exp_shifted(d) * rs;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ NLL
+constexpr int NLL_THREADS = 256;
+
+__global__ void __launch_bounds__(NLL_THREADS)
+    nll_forward_kernel(const float* __restrict__ logp, const int64_t* __restrict__ target,
+                       const float* __restrict__ weight, int64_t N, int64_t C, int64_t ld,
+                       int reduction, int64_t ignore_index, float* loss, float* total_weight,
+                       double* partials, unsigned* ticket) {
+  __shared__ double red[NLL_THREADS / 32];
+  __shared__ unsigned is_last;
+  double num = 0.0, den = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * NLL_THREADS + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * NLL_THREADS) {
+    const int64_t t = target[i];
+    double li = 0.0;
+    if (t != ignore_index) {
+      if (t < 0 || t >= C) {
+        li = __longlong_as_double(0x7ff8000000000000ll);  // reading R17: invalid target -> NaN
+      } else {
+        const double w = weight ? (double)weight[t] : 1.0;
+        li = -w * (double)logp[i * ld + t];
+        den += w;
+      }
+    }
+    if (reduction == NORM_REDUCTION_NONE) loss[i] = (float)li;
+    num += li;
+  }
+  const double bn = block_sum(num, red);
+  const double bd = block_sum(den, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = bn;
+    partials[2 * blockIdx.x + 1] = bd;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double vn = 0.0, vd = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += NLL_THREADS) {
+    vn += __ldcg(partials + 2 * i);
+    vd += __ldcg(partials + 2 * i + 1);
+  }
+  const double Sn = block_sum(vn, red);
+  const double Sd = block_sum(vd, red);
+  if (threadIdx.x == 0) {
+    if (reduction == NORM_REDUCTION_SUM) loss[0] = (float)Sn;
+    if (reduction == NORM_REDUCTION_MEAN) loss[0] = (float)(Sn / Sd);
+    if (total_weight) *total_weight = (float)Sd;
+    *ticket = 0u;
+  }
+}
+
+// grad[i, :] = 0 except grad[i, t_i] = -w[t_i] * g_i / (MEAN ? total_weight : 1).
+template <bool VEC>
+__global__ void __launch_bounds__(256)
+    nll_backward_kernel(float* __restrict__ grad, const float* __restrict__ grad_out,
+                        const int64_t* __restrict__ target, const float* __restrict__ weight,
+                        const float* __restrict__ total_weight, int64_t N, int64_t C, int64_t ld,
+                        int reduction, int64_t ignore_index) {
+  const double tw = reduction == NORM_REDUCTION_MEAN ? (double)*total_weight : 1.0;
+  const double g0 = reduction == NORM_REDUCTION_NONE ? 0.0 : (double)grad_out[0];
+  for (int64_t r = blockIdx.x; r < N; r += gridDim.x) {
+    const int64_t t = target[r];
+    const bool hit = t != ignore_index && t >= 0 && t < C;
+    float val = 0.0f;
+    if (hit) {
+      const double w = weight ? (double)weight[t] : 1.0;
+      const double g = reduction == NORM_REDUCTION_NONE ? (double)grad_out[r] : g0;
+      val = (float)(-w * g / tw);
+    }
+    float* row = grad + r * ld;
+    if constexpr (VEC) {
+      const int64_t nv = C >> 3;
+      for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        f8 z;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) z.v[j] = (hit && v * 8 + j == t) ? val : 0.0f;
+        st8_stream(row + v * 8, z);
+      }
+    } else {
+      for (int64_t c = threadIdx.x; c < C; c += blockDim.x) row[c] = (hit && c == t) ? val : 0.0f;
+    }
+  }
+}
+
+// ============================================================ launchers
+
+cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
+                                int64_t ld_out, int64_t ld_in, bool log, const DeviceInfo& d,
+                                cudaStream_t st) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 31u) == 0 &&
+                       (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
+  const bool vec = aligned && out != in && cols <= (int64_t)SM_THREADS * 8 * 4;
+  const int maxv = cols <= SM_THREADS * 8 ? 1 : (cols <= SM_THREADS * 16 ? 2 : 4);
+  int64_t g = (int64_t)d.sms * (vec ? sm_ctas_per_sm(maxv) : 8);
+  if (rows < g) g = rows;
+#define NORM_SM(LG, M) \
+  softmax_vec_kernel<LG, M><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in)
+  if (!vec) {
+    if (log) softmax_generic_kernel<true><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in);
+    else softmax_generic_kernel<false><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in);
+  } else if (log) {
+    if (maxv == 1) NORM_SM(true, 1);
+    else if (maxv == 2) NORM_SM(true, 2);
+    else NORM_SM(true, 4);
+  } else {
+    if (maxv == 1) NORM_SM(false, 1);
+    else if (maxv == 2) NORM_SM(false, 2);
+    else NORM_SM(false, 4);
+  }
+#undef NORM_SM
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nll_forward(float* loss, float* total_weight, const float* logp,
+                               const int64_t* target, const float* weight, int64_t N, int64_t C,
+                               int64_t ld, int reduction, int64_t ignore_index,
+                               const Workspace& ws, const DeviceInfo& d, cudaStream_t st) {
+  int64_t g = (N + NLL_THREADS - 1) / NLL_THREADS;
+  if (g > (int64_t)d.sms * 4) g = (int64_t)d.sms * 4;
+  if (g > kMaxGrid / 2) g = kMaxGrid / 2;
+  if (g < 1) g = 1;
+  nll_forward_kernel<<<(int)g, NLL_THREADS, 0, st>>>(logp, target, weight, N, C, ld, reduction,
+                                                     ignore_index, loss, total_weight,
+                                                     ws.partials, ws.ticket);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_t* target,
+                                const float* weight, const float* total_weight, int64_t N,
+                                int64_t C, int64_t ld, int reduction, int64_t ignore_index,
+                                const DeviceInfo& d, cudaStream_t st) {
+  const bool vec = (reinterpret_cast<uintptr_t>(grad) & 31u) == 0 && ld % 8 == 0 && C % 8 == 0;
+  int64_t g = (int64_t)d.sms * 8;
+  if (N < g) g = N;
+  int threads = (int)((vec ? C / 8 : C) < 256 ? ((vec ? C / 8 : C) + 31) / 32 * 32 : 256);
+  if (threads < 32) threads = 32;
+  if (vec)
+    nll_backward_kernel<true><<<(int)g, threads, 0, st>>>(grad, grad_out, target, weight,
+                                                          total_weight, N, C, ld, reduction,
+                                                          ignore_index);
+  else
+    nll_backward_kernel<false><<<(int)g, threads, 0, st>>>(grad, grad_out, target, weight,
+                                                           total_weight, N, C, ld, reduction,
+                                                           ignore_index);
+  return cudaGetLastError();
+}
+
+}  // namespace lnorm
