@@ -148,11 +148,21 @@ def dist_setup(args):
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 needs torchrun (one process per GPU)")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("NORM_BENCH_BACKEND", "nccl")  # gloo: harness tests on one GPU
+        dev = local if backend == "nccl" else int(os.environ.get("NORM_BENCH_DEVICE", local))
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def _dev():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 def max_over_ranks(v, world):
@@ -160,9 +170,26 @@ def max_over_ranks(v, world):
     import torch.distributed as dist
     if world == 1:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_dev())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def host_all_gather(world):
+    """All-gather of the 8-byte partial over the default process group (used by
+    --exchange host: norm_shard_partial -> this -> norm_shard_finish)."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(part):
+        if _dev() == "cuda":
+            out = torch.empty(world, dtype=torch.float64, device="cuda")
+            dist.all_gather_into_tensor(out, part)
+            return out
+        lst = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(lst, part.cpu())
+        return torch.cat(lst).cuda()
+    return ag
 
 
 def barrier(world):
@@ -172,6 +199,7 @@ def barrier(world):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+
 
 
 def run_reference(args):
@@ -227,14 +255,17 @@ def run_vector(args, world, rank, local):
         off += ln
     out = torch.empty_like(inp)
     torch.cuda.synchronize()
-    comm = L.Comm() if world > 1 else None
+    comm = L.Comm() if world > 1 and args.exchange == "nccl" else None
+    ag = host_all_gather(world) if world > 1 and args.exchange == "host" else None
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
-        if comm is None:
+        if world == 1:
             L.normalize(out, inp, index=index, path=args.path, events=ev)
-        else:
+        elif comm is not None:
             comm.normalize_sharded(out, inp, mine, n, index=index, events=ev)
+        else:
+            L.normalize_sharded_via(out, inp, mine, n, ag, index=index, events=ev)
 
     for _ in range(args.warmup):
         step()
@@ -260,7 +291,7 @@ def run_vector(args, world, rank, local):
     achieved = red_bytes / (red_ms_avg / 1e3) / 1e9
     extra = {}
     # dense-index figure on the same buffers (caption reading R1), reported beside the headline
-    if args.also_dense and index == "literal":
+    if args.also_dense and index == "literal" and (world == 1 or comm is not None):
         dense_mine = L.plan_shards(n, world, "dense", True)[rank]
         if dense_mine == mine or world == 1:
             for _ in range(2):
@@ -296,14 +327,16 @@ def run_vector(args, world, rank, local):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"normalize n=2^{n.bit_length() - 1} fp32 (Fig. 1), {index} index, "
                                f"{'two-pass' if world > 1 or args.path == 'auto' else args.path}"
-                               + (", coverage-balanced shards + 8 B ncclAllGather" if world > 1 else ""),
+                               + ((", coverage-balanced shards + 8 B " + ("ncclAllGather" if comm else
+                                   "all-gather over the torch.distributed group")) if world > 1 else ""),
                    "n": n, "index": index, "covered": cov_count, "algorithmic_bytes": algo,
-                   "parallelism": f"shard{world}", "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
-                   "l2": "no flush: 16 GiB input >> 126 MB L2"},
+                   "parallelism": f"shard{world}", "exchange": args.exchange if world > 1 else None, "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
+                   "l2": f"no flush: {4 * nloc / 2**30:.1f} GiB input per GPU >> 126 MB L2"},
         "frac_of_hbm_peak": value / (world * peak),
         "frac_of_datasheet": value / (world * DATASHEET_GBS),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": load_traffic("vector", index),
+                     "frac": achieved / peak,
+                     "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
                      "kernel": "reduce_kernel (hoisted sum: 94% of literal bytes)",
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_local, "peak_source": peak_src},
@@ -345,7 +378,8 @@ def run_e2e(args, world, rank, local, mine, n, index):
     stream = torch.cuda.current_stream()
     comm = None
     if world > 1:
-        comm = L.Comm()
+        comm = L.Comm() if args.exchange == "nccl" else None
+        ag = host_all_gather(world)
         din = torch.empty(nloc, dtype=torch.float32, device="cuda")
         dout = torch.empty_like(din)
 
@@ -354,7 +388,10 @@ def run_e2e(args, world, rank, local, mine, n, index):
             L.normalize_host(host_out, host_in, index=index)
         else:
             din.copy_(host_in, non_blocking=True)
-            comm.normalize_sharded(dout, din, mine, n, index=index)
+            if comm is not None:
+                comm.normalize_sharded(dout, din, mine, n, index=index)
+            else:
+                L.normalize_sharded_via(dout, din, mine, n, ag, index=index)
             o = 0
             for b, ln in mine:
                 c = max(0, min(b + ln, prefix) - b)
@@ -380,7 +417,8 @@ def run_e2e(args, world, rank, local, mine, n, index):
     return {"value": algo / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": "norm_launch_host (pinned host buffers, chunked H2D overlapped with the reduce)"
-            if world == 1 else "H2D + norm_launch_sharded + D2H of covered elements"}
+            if world == 1 else ("H2D + norm_launch_sharded + D2H of covered elements" if comm else
+                                "H2D + norm_shard_partial/all-gather/norm_shard_finish + D2H of covered elements")}
 
 
 def run_rows(args, world, rank, local):
@@ -606,11 +644,14 @@ def main():
     ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
-    ap.add_argument("--n", type=int, default=2**32)
+    ap.add_argument("--numel", dest="n", type=int, default=2**32)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--also-dense", action="store_true", default=True)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: norm_launch_sharded (ncclAllGather) or the two-phase API over "
+                         "the torch.distributed process group")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 untimed warm-up steps

@@ -237,6 +237,19 @@ norm_status_t norm_launch_sharded(norm_comm_t* comm, float* out_local, const flo
                                   const norm_shard_t* mine, int64_t n_global,
                                   const norm_opts_t* o);
 
+/* The same path split in two so that any collective can carry the exchange
+ * (e.g. torch.distributed, or a caller-fused kernel):
+ *   norm_shard_partial: *partial (device fp64[1]) <- sum of in_local[0, n_local)
+ *   <caller all-gathers the W partials, in rank order, into a device fp64[W]>
+ *   norm_shard_finish:  s = RN32(partials[0] + ... + partials[W-1]) (rank order),
+ *                       then the scale of the locally covered elements.
+ * norm_launch_sharded == partial + ncclAllGather + finish.  opts as above. */
+norm_status_t norm_shard_partial(double* partial, const float* in_local, int64_t n_local,
+                                 const norm_opts_t* o);
+norm_status_t norm_shard_finish(float* out_local, const float* in_local, const norm_shard_t* mine,
+                                int64_t n_global, const double* partials, int32_t world,
+                                const norm_opts_t* o);
+
 /* -------------------------------------------------------------- errors */
 const char* norm_status_string(norm_status_t s);
 const char* norm_last_error(void);

@@ -27,6 +27,7 @@ from ._lib import (  # noqa: F401
     nll_backward,
     REDUCTION,
     plan_shards,
+    normalize_sharded_via,
     status_string,
     workspace_bytes,
     INDEX,
@@ -35,6 +36,6 @@ from ._lib import (  # noqa: F401
 
 __all__ = [
     "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
-    "plan_shards", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
+    "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

@@ -62,6 +62,8 @@ def lib():
             "norm_comm_destroy": [vp],
             "norm_plan_shards": [i64, i32, i32, i32, ctypes.POINTER(NormShard)],
             "norm_launch_sharded": [vp, vp, vp, ctypes.POINTER(NormShard), i64, optp],
+            "norm_shard_partial": [vp, vp, i64, optp],
+            "norm_shard_finish": [vp, vp, ctypes.POINTER(NormShard), i64, vp, i32, optp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -286,6 +288,29 @@ def _shard_struct(ranges):
         s.begin[k] = b
         s.len[k] = ln
     return s
+
+
+def normalize_sharded_via(out_local, in_local, ranges, n_global, all_gather, index="literal",
+                          stream=None, sum_out=None, sum_out_f64=None, events=None):
+    """The sharded path with a caller-supplied exchange (norm_shard_partial ->
+    all_gather(partial: 1-element float64 CUDA tensor) -> float64 CUDA tensor of the W
+    partials in rank order -> norm_shard_finish).  E.g. torch.distributed over gloo."""
+    import torch
+    _check_f32(out_local, "out_local")
+    _check_f32(in_local, "in_local")
+    if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
+        raise ValueError("local buffers must hold exactly the shard's elements")
+    part = torch.empty(1, dtype=torch.float64, device=in_local.device)
+    o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
+    _check(lib().norm_shard_partial(part.data_ptr(), in_local.data_ptr(), in_local.numel(),
+                                    ctypes.byref(o)))
+    parts = all_gather(part)
+    if parts.dtype != torch.float64 or not parts.is_cuda or not parts.is_contiguous():
+        raise ValueError("all_gather must return a contiguous float64 CUDA tensor")
+    shard = _shard_struct(ranges)
+    _check(lib().norm_shard_finish(out_local.data_ptr(), in_local.data_ptr(), ctypes.byref(shard),
+                                   n_global, parts.data_ptr(), parts.numel(), ctypes.byref(o)))
+    return out_local
 
 
 class Comm:

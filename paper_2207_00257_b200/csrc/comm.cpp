@@ -127,69 +127,63 @@ NORM_API norm_status_t norm_plan_shards(int64_t n, int32_t world, int32_t index,
   return NORM_OK;
 }
 
-NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, const float* in_local,
-                                           const norm_shard_t* mine, int64_t n_global,
-                                           const norm_opts_t* o) {
-  static const norm_opts_t kDef = NORM_OPTS_INIT;
-  if (!o) o = &kDef;
-  if (!c || !mine) return fail(NORM_ERR_INVALID_VALUE, "comm or shard is NULL");
+// Validate a shard; *local = number of local elements.
+static norm_status_t check_shard(float* out_local, const float* in_local, const norm_shard_t* mine,
+                                 int64_t n_global, const norm_opts_t* o, int64_t* local) {
+  if (!mine) return fail(NORM_ERR_INVALID_VALUE, "shard is NULL");
   if (o->index != NORM_INDEX_LITERAL && o->index != NORM_INDEX_DENSE)
     return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
   if (n_global < 0 || mine->nranges < 0 || mine->nranges > 2)
     return fail(NORM_ERR_INVALID_VALUE, "bad shard");
-  int64_t local = 0, prev_end = 0;
+  int64_t n = 0, prev_end = 0;
   for (int k = 0; k < mine->nranges; ++k) {
     if (mine->len[k] < 0 || mine->begin[k] < prev_end || mine->begin[k] + mine->len[k] > n_global)
       return fail(NORM_ERR_INVALID_VALUE, "shard ranges must be ascending, disjoint, inside [0, n)");
     prev_end = mine->begin[k] + mine->len[k];
-    local += mine->len[k];
+    n += mine->len[k];
   }
-  if (local > 0) {
+  if (n > 0) {
     if (!out_local || !in_local) return fail(NORM_ERR_INVALID_VALUE, "NULL local buffer");
     if ((reinterpret_cast<uintptr_t>(out_local) | reinterpret_cast<uintptr_t>(in_local)) & 3u)
       return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
     uintptr_t a = reinterpret_cast<uintptr_t>(out_local), b = reinterpret_cast<uintptr_t>(in_local);
-    if (a != b && a < b + local * 4 && b < a + local * 4)
+    if (a != b && a < b + n * 4 && b < a + n * 4)
       return fail(NORM_ERR_OVERLAP, "out_local and in_local partially overlap");
   }
   const Coverage cov = coverage_of(n_global, o->index);
   if (o->index == NORM_INDEX_LITERAL && cov.G > 2147483647LL)
     return fail(NORM_ERR_UNSUPPORTED, "literal launch needs > 2^31-1 blocks");
-  DeviceInfo d;
-  std::string err;
-  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
-  if (d.device != c->device) return fail(NORM_ERR_INVALID_VALUE, "current device != comm device");
-  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
-  Workspace ws = workspace_carve(c->ws);
+  *local = n;
+  return NORM_OK;
+}
 
-  // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
-  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  cudaError_t e = launch_reduce(in_local, local, ws, c->send, reduce_grid(d, local), st);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
-  // 2. exchange: W x 8 bytes over NVLink
-  ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
-  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-  // 3. scale the locally covered elements; the prologue combines recv[0..W) in rank order
+// Step 3 of the sharded path: combine the W partials in rank order (scale
+// prologue) and scale the locally covered elements of each owned range.
+static norm_status_t shard_finish(float* out_local, const float* in_local, const norm_shard_t* mine,
+                                  int64_t n_global, const double* partials, int world,
+                                  const norm_opts_t* o, const DeviceInfo& d) {
+  const Coverage cov = coverage_of(n_global, o->index);
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   float* so = o->sum_out;
   double* so64 = o->sum_out_f64;
   int64_t off = 0;
   bool launched = false;
+  cudaError_t e;
   for (int k = 0; k < mine->nranges; ++k) {
     const int64_t gb = mine->begin[k], len = mine->len[k];
     if (cov.kind == COV_PREFIX) {
-      int64_t ce = gb + len < cov.L ? gb + len : cov.L;
-      int64_t clen = ce > gb ? ce - gb : 0;
+      const int64_t ce = gb + len < cov.L ? gb + len : cov.L;
+      const int64_t clen = ce > gb ? ce - gb : 0;
       if (clen > 0) {
-        e = launch_scale(out_local + off, in_local + off, clen, c->recv, c->world, so, so64, d, false, st);
+        e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, false, st);
         if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
         so = nullptr;
         so64 = nullptr;
         launched = true;
       }
     } else if (cov.kind == COV_RESIDUE && len > 0) {
-      e = launch_scale_residue(out_local + off, in_local + off, len, gb, cov.G, c->recv, c->world,
-                               so, so64, false, st);
+      e = launch_scale_residue(out_local + off, in_local + off, len, gb, cov.G, partials, world, so,
+                               so64, false, st);
       if (e != cudaSuccess) return cuda_fail(e, "scale_residue launch");
       so = nullptr;
       so64 = nullptr;
@@ -198,8 +192,73 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
     off += len;
   }
   if (!launched && (so || so64)) {  // nothing covered here, but the caller wants s
-    e = launch_scale(out_local, in_local, 0, c->recv, c->world, so, so64, d, false, st);
+    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, false, st);
     if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
   }
   return NORM_OK;
+}
+
+NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, const float* in_local,
+                                           const norm_shard_t* mine, int64_t n_global,
+                                           const norm_opts_t* o) {
+  static const norm_opts_t kDef = NORM_OPTS_INIT;
+  if (!o) o = &kDef;
+  if (!c) return fail(NORM_ERR_INVALID_VALUE, "comm is NULL");
+  int64_t local = 0;
+  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  if (s != NORM_OK) return s;
+  DeviceInfo d;
+  std::string err;
+  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if (d.device != c->device) return fail(NORM_ERR_INVALID_VALUE, "current device != comm device");
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Workspace ws = workspace_carve(c->ws);
+  // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
+  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  cudaError_t e = launch_reduce(in_local, local, ws, c->send, reduce_grid(d, local), st);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  // 2. exchange: W x 8 bytes over NVLink
+  ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  // 3. rank-order combine + scale
+  return shard_finish(out_local, in_local, mine, n_global, c->recv, c->world, o, d);
+}
+
+NORM_API norm_status_t norm_shard_partial(double* partial, const float* in_local, int64_t n_local,
+                                          const norm_opts_t* o) {
+  static const norm_opts_t kDef = NORM_OPTS_INIT;
+  if (!o) o = &kDef;
+  if (!partial || n_local < 0 || (n_local > 0 && !in_local))
+    return fail(NORM_ERR_INVALID_VALUE, "bad partial arguments");
+  if (reinterpret_cast<uintptr_t>(in_local) & 3u)
+    return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  DeviceInfo d;
+  std::string err;
+  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Workspace ws;
+  norm_status_t s = get_workspace(o, d.device, st, &ws);
+  if (s != NORM_OK) return s;
+  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  cudaError_t e = launch_reduce(in_local, n_local, ws, partial, reduce_grid(d, n_local), st);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_shard_finish(float* out_local, const float* in_local,
+                                         const norm_shard_t* mine, int64_t n_global,
+                                         const double* partials, int32_t world,
+                                         const norm_opts_t* o) {
+  static const norm_opts_t kDef = NORM_OPTS_INIT;
+  if (!o) o = &kDef;
+  if (!partials || world < 1) return fail(NORM_ERR_INVALID_VALUE, "bad partials");
+  int64_t local = 0;
+  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  if (s != NORM_OK) return s;
+  DeviceInfo d;
+  std::string err;
+  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  return shard_finish(out_local, in_local, mine, n_global, partials, world, o, d);
 }

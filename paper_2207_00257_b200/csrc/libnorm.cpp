@@ -151,7 +151,7 @@ static norm_status_t internal_workspace(int dev, cudaStream_t st, Workspace* ws)
   return NORM_OK;
 }
 
-static norm_status_t get_workspace(const norm_opts_t* o, int dev, cudaStream_t st, Workspace* ws) {
+norm_status_t get_workspace(const norm_opts_t* o, int dev, cudaStream_t st, Workspace* ws) {
   if (o->workspace) {
     if (o->workspace_bytes < workspace_bytes())
       return fail(NORM_ERR_WORKSPACE, "workspace_bytes < norm_workspace_bytes()");

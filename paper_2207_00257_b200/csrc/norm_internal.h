@@ -33,6 +33,8 @@ struct Workspace {
 };
 size_t workspace_bytes();
 Workspace workspace_carve(void* base);
+// o->workspace if given (checked), else the internal (device, stream) cache.
+norm_status_t get_workspace(const norm_opts_t* o, int dev, cudaStream_t st, Workspace* ws);
 
 struct DeviceInfo {
   int device;
