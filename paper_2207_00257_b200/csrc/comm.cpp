@@ -215,7 +215,7 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
   Workspace ws = workspace_carve(c->ws);
   // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
   if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  cudaError_t e = launch_reduce(in_local, local, ws, c->send, reduce_grid(d, local), st);
+  cudaError_t e = launch_reduce(in_local, local, ws, c->send, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   // 2. exchange: W x 8 bytes over NVLink
@@ -241,7 +241,7 @@ NORM_API norm_status_t norm_shard_partial(double* partial, const float* in_local
   norm_status_t s = get_workspace(o, d.device, st, &ws);
   if (s != NORM_OK) return s;
   if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  cudaError_t e = launch_reduce(in_local, n_local, ws, partial, reduce_grid(d, n_local), st);
+  cudaError_t e = launch_reduce(in_local, n_local, ws, partial, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   return NORM_OK;

@@ -71,6 +71,7 @@ template <int THREADS, int UNROLL, bool VEC, bool ALIAS>
 __device__ __forceinline__ void scale_segment(float* out, const float* in, int64_t len, float s,
                                               int cta, int ncta) {
   if (len <= 0) return;
+  const float rs = __frcp_rn(s);
   if constexpr (VEC) {
     const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(out) & 31u);
     int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
@@ -88,22 +89,22 @@ __device__ __forceinline__ void scale_segment(float* out, const float* in, int64
         v[u] = ALIAS ? ld8(ib + off + (int64_t)u * THREADS * 8)
                      : ld8_stream(ib + off + (int64_t)u * THREADS * 8);
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], s));
+      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], s, rs));
     }
     for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
          vi += (int64_t)ncta * THREADS) {
       f8 v = ALIAS ? ld8(ib + vi * 8) : ld8_stream(ib + vi * 8);
-      st8_stream(ob + vi * 8, div8(v, s));
+      st8_stream(ob + vi * 8, div8(v, s, rs));
     }
     if (cta == 0) {
-      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], s);
+      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], s, rs);
       const int64_t t = head + nv * 8 + threadIdx.x;
-      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], s);
+      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], s, rs);
     }
   } else {
     const int64_t stride = (int64_t)ncta * THREADS;
     for (int64_t i = (int64_t)cta * THREADS + threadIdx.x; i < len; i += stride)
-      out[i] = div_rn(in[i], s);
+      out[i] = div_rn(in[i], s, rs);
   }
 }
 
@@ -135,6 +136,96 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     *S_out = S;
     *ticket = 0u;  // leave the workspace reusable
+  }
+}
+
+// Pass 1, TMA-bulk variant for large n: one CTA per SM; warp 0 (one elected
+// lane) streams 32 KiB chunks of the 16-byte-aligned body into a 4-stage
+// shared-memory ring with cp.async.bulk (128 KiB in flight per SM, the measured
+// sweet spot of scripts/microbench_reduce.cu: 7.56 TB/s vs 7.29 TB/s for the
+// best LDG.E.256 geometry); 8 consumer warps sum each landed chunk from shared
+// memory (fixed per-thread order), then release the stage.  Chunks are dealt
+// grid-strided; the < 32 KiB remainder and the < 16 B head go through LDG.
+constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32, BK_STAGES = 4;
+constexpr int BK_CHUNK = 32768;  // bytes per stage
+constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernel is as fast
+
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                       unsigned* __restrict__ ticket, double* __restrict__ S_out) {
+  pdl_launch_dependents();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ double red[BK_THREADS / 32];
+  __shared__ unsigned is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // split: head (to 16 B) | body of whole 32 KiB chunks | remainder
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(in) & 15u);
+  int64_t head = (int64_t)(((16u - mis) & 15u) >> 2);
+  if (head > n) head = n;
+  const float* body = in + head;
+  constexpr int64_t CF = BK_CHUNK / 4;  // floats per chunk
+  const int64_t nchunks = (n - head) / CF;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < BK_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], BK_CONSUMERS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double acc = 0.0;
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int s = 0, it = 0;
+      unsigned ph = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        if (it >= BK_STAGES) mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], BK_CHUNK);
+        bulk_g2s(ring + (size_t)s * BK_CHUNK, body + c * CF, BK_CHUNK, &full[s]);
+        if (++s == BK_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {  // consumers
+    const int ct = threadIdx.x - 32;
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      mbar_wait(&full[s], ph);
+      const float4* p = reinterpret_cast<const float4*>(ring + (size_t)s * BK_CHUNK);
+#pragma unroll
+      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+        const int i = k * BK_CONSUMERS + ct;  // 8-float group i of the chunk
+        const float4 a = p[2 * i], b = p[2 * i + 1];
+        f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+        acc += sum8(v);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == BK_STAGES) { s = 0; ph ^= 1; }
+    }
+    // remainder after the whole chunks, and the head: plain loads
+    const int64_t rbeg = head + nchunks * CF;
+    for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < n;
+         i += (int64_t)gridDim.x * BK_CONSUMERS)
+      acc += (double)__ldg(in + i);
+    if (blockIdx.x == 0 && ct < head) acc += (double)__ldg(in + ct);
+  }
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    *S_out = S;
+    *ticket = 0u;
   }
 }
 
@@ -284,7 +375,7 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
   for (int k = 0; k < MAXV; ++k)
     if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
   const double S = block_sum(acc, red);
-  const float s = (float)S;
+  const float s = (float)S, rs = __frcp_rn(s);
   if (threadIdx.x == 0) {
     if (sum_out) sum_out[r] = s;
     if (sum_out_f64) sum_out_f64[r] = S;
@@ -295,11 +386,11 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
     if (idx >= nvr) continue;
     const int64_t e0 = (int64_t)idx * 8;
     if (L >= 0 && e0 + 8 <= L) {
-      st8_stream(dst + e0, div8(v[k], s));
+      st8_stream(dst + e0, div8(v[k], s, rs));
     } else if (L < 0 || e0 < L) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s);
+        if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s, rs);
     }
   }
 }
@@ -361,8 +452,20 @@ int reduce_grid(const DeviceInfo& d, int64_t n) {
 }
 
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          int grid, cudaStream_t st) {
-  reduce_kernel<<<grid, RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out);
+                          const DeviceInfo& d, cudaStream_t st) {
+  if (n >= kBulkMinN) {
+    static int configured[64] = {0};  // per device: opt in to 128 KiB of dynamic smem
+    const size_t smem = (size_t)BK_STAGES * BK_CHUNK;
+    if (d.device < 64 && !configured[d.device]) {
+      cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      configured[d.device] = 1;
+    }
+    reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out);
+    return cudaGetLastError();
+  }
+  reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out);
   return cudaGetLastError();
 }
 

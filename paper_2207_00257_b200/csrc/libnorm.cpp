@@ -239,7 +239,7 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
     return e == cudaSuccess ? NORM_OK : cuda_fail(e, "fused_kernel cooperative launch");
   }
   if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  e = launch_reduce(in, cov.n, ws, ws.S, reduce_grid(d, cov.n), st);
+  e = launch_reduce(in, cov.n, ws, ws.S, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   if (cov.kind == COV_PREFIX)
@@ -366,7 +366,7 @@ static norm_status_t launch_host(float* out_host, const float* in_host, const Co
     cudaEvent_t landed = h->landed[k & 1];
     if ((e = cudaEventRecord(landed, h->copy)) != cudaSuccess) return cuda_fail(e, "event record");
     if ((e = cudaStreamWaitEvent(st, landed, 0)) != cudaSuccess) return cuda_fail(e, "wait");
-    if ((e = launch_reduce(dst, len, ws, h->chunkS + k, reduce_grid(d, len), st)) != cudaSuccess)
+    if ((e = launch_reduce(dst, len, ws, h->chunkS + k, d, st)) != cudaSuccess)
       return cuda_fail(e, "reduce_kernel launch");
     if (used_slot >= 0 && (e = cudaEventRecord(h->slot_free[used_slot], st)) != cudaSuccess)
       return cuda_fail(e, "event record");

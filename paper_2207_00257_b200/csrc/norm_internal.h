@@ -50,8 +50,9 @@ bool device_info(DeviceInfo* out, std::string* err);
 int reduce_grid(const DeviceInfo& d, int64_t n);
 
 // S_out <- sum of in[0, n) (fp64), via per-CTA partials and a last-block ticket.
+// n >= 2^22: TMA-bulk kernel (one CTA per SM); smaller n: LDG.E.256 kernel.
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          int grid, cudaStream_t st);
+                          const DeviceInfo& d, cudaStream_t st);
 
 // out[i] = in[i] / s for i in [0, len), s = (float)(S_parts[0] + ... + S_parts[nparts-1])
 // (fixed order).  Launched as a PDL dependent of the preceding kernel when pdl.

@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(T, MINB) red_ldg(const float* in, int64_t nv, 
 
 // TMA 1-D bulk copies into a ring of shared-memory stages (one elected producer
 // thread), consumer warps sum from shared memory.
-template <int T, int STAGES, int STAGE_BYTES>
-__global__ void __launch_bounds__(T, 1) red_bulk(const float* in, int64_t nbytes_total, double* out) {
+template <int T, int STAGES, int STAGE_BYTES, int MINB = 1, bool CONTIG = false>
+__global__ void __launch_bounds__(T, MINB) red_bulk(const float* in, int64_t nbytes_total, double* out) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
   __shared__ double red[T / 32];
@@ -62,7 +62,11 @@ __global__ void __launch_bounds__(T, 1) red_bulk(const float* in, int64_t nbytes
       int s = 0;
       unsigned ph = 0;
       int it = 0;
-      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+      const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+      const int64_t c0 = CONTIG ? blockIdx.x * per : blockIdx.x;
+      const int64_t c1 = CONTIG ? (c0 + per < nchunks ? c0 + per : nchunks) : nchunks;
+      const int64_t cs = CONTIG ? 1 : gridDim.x;
+      for (int64_t c = c0; c < c1; c += cs, ++it) {
         if (it >= STAGES) {
           unsigned b = (unsigned)__cvta_generic_to_shared(&empty[s]);
           asm volatile(
@@ -83,7 +87,11 @@ __global__ void __launch_bounds__(T, 1) red_bulk(const float* in, int64_t nbytes
     int s = 0;
     unsigned ph = 0;
     const int cw = warp - 1, ncw = T / 32 - 1;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = CONTIG ? blockIdx.x * per : blockIdx.x;
+    const int64_t c1 = CONTIG ? (c0 + per < nchunks ? c0 + per : nchunks) : nchunks;
+    const int64_t cs = CONTIG ? 1 : gridDim.x;
+    for (int64_t c = c0; c < c1; c += cs) {
       unsigned fb = (unsigned)__cvta_generic_to_shared(&full[s]);
       asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(fb),
                    "r"(ph));
@@ -99,6 +107,29 @@ __global__ void __launch_bounds__(T, 1) red_bulk(const float* in, int64_t nbytes
       }
       if (++s == STAGES) { s = 0; ph ^= 1; }
     }
+  }
+  double b = block_sum(acc, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = b;
+}
+
+template <int T, int U, int MINB, int AHEAD>
+__global__ void __launch_bounds__(T, MINB) red_ldg_pf(const float* in, int64_t nv, double* out) {
+  __shared__ double red[T / 32];
+  double acc = 0;
+  constexpr int64_t CH = (int64_t)T * U;
+  const int64_t nfull = nv / CH;
+  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const int64_t cp = c + (int64_t)AHEAD * gridDim.x;
+      if (cp < nfull)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(in + cp * CH * 8), "r"((int)(CH * 32)) : "memory");
+    }
+    const float* q = in + (c * CH + threadIdx.x) * 8;
+    f8 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld8_stream(q + (int64_t)u * T * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += sum8(v[u]);
   }
   double b = block_sum(acc, red);
   if (threadIdx.x == 0) out[blockIdx.x] = b;
@@ -141,25 +172,28 @@ int main() {
     printf("%-40s %8.3f ms %8.1f GB/s\n", NAME, ms, bytes / ms / 1e6);                  \
   }
   RUN("ldg256 512x2 U4 (current)", 512, 4, 2, false, 2);
-  RUN("ldg256 512x2 U4 L2::256B", 512, 4, 2, true, 2);
-  RUN("ldg256 256x4 U4", 256, 4, 4, false, 4);
-  RUN("ldg256 256x3 U8", 256, 8, 3, false, 3);
-  RUN("ldg256 1024x1 U4", 1024, 4, 1, false, 1);
-  RUN("ldg256 512x2 U2", 512, 2, 2, false, 2);
-  RUN("ldg256 128x8 U4", 128, 4, 8, false, 8);
-  RUN("ldg256 256x4 U4 L2::256B", 256, 4, 4, true, 4);
-  RUN("ldg256 512x1 U8", 512, 8, 1, false, 1);
-#define RUNB(NAME, T, ST, SB)                                                                   \
-  {                                                                                             \
-    cudaFuncSetAttribute(red_bulk<T, ST, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * SB); \
-    float ms = timeit([&] { red_bulk<T, ST, SB><<<sms, T, ST * SB>>>(in, n * 4, out); });        \
-    cudaError_t e = cudaGetLastError();                                                         \
-    printf("%-40s %8.3f ms %8.1f GB/s %s\n", NAME, ms, bytes / ms / 1e6, cudaGetErrorString(e)); \
+#define RUNB2(NAME, T, ST, SB, MB, CG)                                                               \
+  {                                                                                                \
+    cudaFuncSetAttribute(red_bulk<T, ST, SB, MB, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * SB); \
+    float ms = timeit([&] { red_bulk<T, ST, SB, MB, CG><<<sms * MB, T, ST * SB>>>(in, n * 4, out); });       \
+    cudaError_t e = cudaGetLastError();                                                            \
+    printf("%-40s %8.3f ms %8.1f GB/s %s\n", NAME, ms, bytes / ms / 1e6, cudaGetErrorString(e));   \
   }
-  RUNB("bulk 288thr 8x16KiB", 288, 8, 16384);
-  RUNB("bulk 288thr 6x32KiB", 288, 6, 32768);
-  RUNB("bulk 544thr 12x16KiB", 544, 12, 16384);
-  RUNB("bulk 544thr 4x48KiB", 544, 4, 49152);
+  RUNB2("bulk 288 6x16KiB", 288, 6, 16384, 1, false);
+  RUNB2("bulk 288 7x16KiB", 288, 7, 16384, 1, false);
+  RUNB2("bulk 288 8x16KiB", 288, 8, 16384, 1, false);
+  RUNB2("bulk 288 9x16KiB", 288, 9, 16384, 1, false);
+  RUNB2("bulk 288 10x16KiB", 288, 10, 16384, 1, false);
+  RUNB2("bulk 288 16x8KiB", 288, 16, 8192, 1, false);
+  RUNB2("bulk 288 20x8KiB", 288, 20, 8192, 1, false);
+  RUNB2("bulk 288 4x32KiB", 288, 4, 32768, 1, false);
+  RUNB2("bulk 160 8x16KiB", 160, 8, 16384, 1, false);
+  RUNB2("bulk 544 8x16KiB", 544, 8, 16384, 1, false);
+  RUNB2("bulk 288 8x16KiB contig", 288, 8, 16384, 1, true);
+  RUNB2("bulk 288 6x16KiB contig", 288, 6, 16384, 1, true);
+  RUNB2("bulk 288 12x16KiB contig", 288, 12, 16384, 1, true);
+  RUNB2("bulk 2x160 4x16KiB", 160, 4, 16384, 2, false);
+  RUNB2("bulk 2x160 4x16KiB contig", 160, 4, 16384, 2, true);
   // copy-rate reference: cudaMemcpy D2D of 8 GiB (read+write counted)
   float* o2;
   cudaMalloc(&o2, n * 2);

@@ -1,0 +1,161 @@
+// scripts/microbench_scale.cu — design-space probe for libnorm's scale kernel (not
+// product code): out[i] = in[i] / s over n fp32 (a copy-like HBM stream) with
+// several load/store schemes; prints GB/s (read + write bytes).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//        -I paper_2207_00257_b200/csrc scripts/microbench_scale.cu -o scripts/mb_scale
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "device_common.cuh"
+
+using namespace lnorm;
+
+template <int T, int U, int MINB>
+__global__ void __launch_bounds__(T, MINB) sc_ldg(float* out, const float* in, int64_t nv, float s) {
+  constexpr int64_t CH = (int64_t)T * U;
+  const int64_t nfull = nv / CH;
+  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x) {
+    const int64_t off = (c * CH + threadIdx.x) * 8;
+    f8 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld8_stream(in + off + (int64_t)u * T * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st8_stream(out + off + (int64_t)u * T * 8, div8(v[u], s));
+  }
+}
+
+// plain (non-.cs) stores
+__device__ __forceinline__ void st8_plain(float* p, const f8& r) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+               "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+               : "memory");
+}
+
+template <int T, int U, int MINB>
+__global__ void __launch_bounds__(T, MINB) sc_ldg_plainst(float* out, const float* in, int64_t nv, float s) {
+  constexpr int64_t CH = (int64_t)T * U;
+  const int64_t nfull = nv / CH;
+  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x) {
+    const int64_t off = (c * CH + threadIdx.x) * 8;
+    f8 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld8_stream(in + off + (int64_t)u * T * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st8_plain(out + off + (int64_t)u * T * 8, div8(v[u], s));
+  }
+}
+
+// bulk loads into a smem ring, consumers divide and store with STG.256.
+template <int NC, int ST, int CB>
+__global__ void __launch_bounds__(NC + 32, 1) sc_bulk(float* out, const float* in, int64_t n, float s) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int64_t CF = CB / 4;
+  const int64_t nchunks = n / CF;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NC / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0, it = 0;
+      unsigned ph = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        if (it >= ST) mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], CB);
+        bulk_g2s(ring + (size_t)st * CB, in + c * CF, CB, &full[st]);
+        if (++st == ST) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    const int ct = threadIdx.x - 32;
+    int st = 0;
+    unsigned ph = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      mbar_wait(&full[st], ph);
+      const float4* p = reinterpret_cast<const float4*>(ring + (size_t)st * CB);
+      float* o = out + c * CF;
+#pragma unroll
+      for (int k = 0; k < CB / 32 / NC; ++k) {
+        const int i = k * NC + ct;
+        const float4 a = p[2 * i], b = p[2 * i + 1];
+        f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+        st8_stream(o + (int64_t)i * 8, div8(v, s));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == ST) { st = 0; ph ^= 1; }
+    }
+  }
+}
+
+template <typename F>
+float timeit(F f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  f();
+  f();
+  float best = 1e30f;
+  for (int i = 0; i < 6; ++i) {
+    cudaEventRecord(a);
+    f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main() {
+  const int64_t n = 1ll << 31;  // 8 GiB in, 8 GiB out
+  float *in, *out;
+  if (cudaMalloc(&in, n * 4) != cudaSuccess || cudaMalloc(&out, n * 4) != cudaSuccess) {
+    printf("alloc failed\n");
+    return 1;
+  }
+  cudaMemset(in, 0x3F, n * 4);  // 0x3F3F3F3F = 0.747f (zeros take __fdiv_rn's slow path)
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const double bytes = 8.0 * n;
+  const int64_t nv = n / 8;
+  const float s = 3.0f;
+#define RUN(NAME, K, T, CTAS)                                                     \
+  {                                                                             \
+    float ms = timeit([&] { K<<<sms * CTAS, T>>>(out, in, nv, s); });           \
+    printf("%-42s %8.3f ms %8.1f GB/s\n", NAME, ms, bytes / ms / 1e6);          \
+  }
+  RUN("ldg/stg.cs 256x4 U4 (current)", (sc_ldg<256, 4, 4>), 256, 4);
+  RUN("ldg/stg.cs 512x2 U4", (sc_ldg<512, 4, 2>), 512, 2);
+  RUN("ldg/stg.cs 256x4 U2", (sc_ldg<256, 2, 4>), 256, 4);
+  RUN("ldg/stg.cs 256x6 U2", (sc_ldg<256, 2, 6>), 256, 6);
+  RUN("ldg/stg.cs 256x8 U2", (sc_ldg<256, 2, 8>), 256, 8);
+  RUN("ldg/stg.cs 1024x1 U4", (sc_ldg<1024, 4, 1>), 1024, 1);
+  RUN("ldg/stg 256x4 U4 (plain st)", (sc_ldg_plainst<256, 4, 4>), 256, 4);
+  RUN("ldg/stg 512x2 U2 (plain st)", (sc_ldg_plainst<512, 2, 2>), 512, 2);
+#define RUNB(NAME, NC, ST, CB)                                                                  \
+  {                                                                                             \
+    cudaFuncSetAttribute(sc_bulk<NC, ST, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CB); \
+    float ms = timeit([&] { sc_bulk<NC, ST, CB><<<sms, NC + 32, ST * CB>>>(out, in, n, s); });   \
+    printf("%-42s %8.3f ms %8.1f GB/s %s\n", NAME, ms, bytes / ms / 1e6,                        \
+           cudaGetErrorString(cudaGetLastError()));                                             \
+  }
+  RUNB("bulk-load 256c 4x32KiB + stg.cs", 256, 4, 32768);
+  RUNB("bulk-load 256c 8x16KiB + stg.cs", 256, 8, 16384);
+  RUNB("bulk-load 512c 4x32KiB + stg.cs", 512, 4, 32768);
+  RUNB("bulk-load 256c 3x32KiB + stg.cs", 256, 3, 32768);
+  RUNB("bulk-load 256c 6x32KiB + stg.cs", 256, 6, 32768);
+  cudaMemset(in, 0, n * 4);  // all-zero dividends: must not fall to the slow path
+  RUN("ldg/stg.cs 256x4 U4, zero input", (sc_ldg<256, 4, 4>), 256, 4);
+  cudaMemset(in, 0x3F, n * 4);
+  float ms = timeit([&] { cudaMemcpyAsync(out, in, n * 4, cudaMemcpyDeviceToDevice); });
+  printf("%-42s %8.3f ms %8.1f GB/s\n", "cudaMemcpy D2D", ms, bytes / ms / 1e6);
+  return 0;
+}

@@ -442,3 +442,23 @@ def test_torch_ops():
     assert torch.allclose(f(m), r, rtol=1e-6, atol=0)
     with pytest.raises(RuntimeError):
         torch.ops.libnorm.normalize(torch.ones(4), "dense")
+
+
+def test_signed_zeros_and_zero_heavy():
+    """Zero dividends take a dedicated branch in the scale (div_rn): the sign of
+    every zero quotient must still be IEEE's, for both signs of the divisor."""
+    n = 2**20 + 7
+    base = gen.make_host(n, seed=12, dist="signed")
+    for frac_zero in (0.5, 0.99):
+        x = base.copy()
+        m = gen.make_host(n, seed=13, dist="unit") < frac_zero
+        x[m] = np.where(gen.make_host(n, seed=14, dist="unit")[m] < 0.5, np.float32(0.0), np.float32(-0.0))
+        for sign in (1, -1):
+            xs = (x * np.float32(sign)).astype(np.float32)
+            if sign < 0:
+                xs[m] = -xs[m]  # keep a mix of +0 / -0 either way
+            for mode in ("literal", "dense"):
+                for path in ("two_pass", "fused", "small"):
+                    out, s, _ = run(xs, mode, path)
+                    rep = oracle.replay(xs, s, mode, out=sentinel(n))
+                    assert out.view(np.uint32).tobytes() == rep.view(np.uint32).tobytes()
