@@ -17,7 +17,6 @@ namespace lnorm {
 // ------------------------------------------------------------------ tuning
 constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
 constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
-constexpr int FU_THREADS = 512, FU_UNROLL = 4;
 constexpr int SMALL_THREADS = 1024;
 constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 4;
 constexpr int FU_SCALE_UNROLL = 2;
@@ -139,33 +138,90 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
   }
 }
 
-// Pass 1, TMA-bulk variant for large n: one CTA per SM; warp 0 (one elected
-// lane) streams 32 KiB chunks of the 16-byte-aligned body into a 4-stage
-// shared-memory ring with cp.async.bulk (128 KiB in flight per SM, the measured
-// sweet spot of scripts/microbench_reduce.cu: 7.56 TB/s vs 7.29 TB/s for the
-// best LDG.E.256 geometry); 8 consumer warps sum each landed chunk from shared
-// memory (fixed per-thread order), then release the stage.  Chunks are dealt
-// grid-strided; the < 32 KiB remainder and the < 16 B head go through LDG.
+// ---- TMA-bulk streaming sum (cp.async.bulk + mbarrier ring) ----------------
+// One CTA per SM; warp 0 (one elected lane) streams 32 KiB chunks of a segment's
+// 16-byte-aligned body into a 4-stage shared-memory ring (128 KiB in flight per
+// SM: the measured sweet spot of scripts/microbench_reduce.cu, 7.56 TB/s vs
+// 7.29 TB/s for the best LDG.E.256 geometry; deeper rings lose); 8 consumer
+// warps sum each landed chunk from shared memory in a fixed per-thread order and
+// release the stage.  Chunks are dealt grid-strided; the < 32 KiB remainder and
+// the < 16 B head of each segment go through plain loads.  The ring state
+// carries across segments, so a kernel can stream several segments in a row.
 constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32, BK_STAGES = 4;
-constexpr int BK_CHUNK = 32768;  // bytes per stage
+constexpr int BK_CHUNK = 32768;        // bytes per stage
+constexpr int64_t BK_CF = BK_CHUNK / 4;  // floats per stage
+constexpr size_t BK_SMEM = (size_t)BK_STAGES * BK_CHUNK;
 constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernel is as fast
 
-__global__ void __launch_bounds__(BK_THREADS, 1)
-    reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
-                       unsigned* __restrict__ ticket, double* __restrict__ S_out) {
-  pdl_launch_dependents();
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
-  __shared__ double red[BK_THREADS / 32];
-  __shared__ unsigned is_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // split: head (to 16 B) | body of whole 32 KiB chunks | remainder
-  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(in) & 15u);
-  int64_t head = (int64_t)(((16u - mis) & 15u) >> 2);
-  if (head > n) head = n;
-  const float* body = in + head;
-  constexpr int64_t CF = BK_CHUNK / 4;  // floats per chunk
-  const int64_t nchunks = (n - head) / CF;
+struct BulkRing {
+  unsigned char* buf;
+  uint64_t* full;
+  uint64_t* empty;
+  int stage;
+  unsigned phase;
+  int issued;
+  __device__ __forceinline__ void advance() {
+    if (++stage == BK_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+__device__ __forceinline__ void bulk_split(const float* p, int64_t len, int64_t* head, int64_t* nchunks) {
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 15u);
+  int64_t h = (int64_t)(((16u - mis) & 15u) >> 2);
+  if (h > len) h = len;
+  *head = h;
+  *nchunks = (len - h) / BK_CF;
+}
+
+// Producer side (call from one lane): issue this CTA's chunks of [p, p + len).
+template <bool HINT>
+__device__ __forceinline__ void bulk_produce(BulkRing& r, const float* p, int64_t len, uint64_t pol) {
+  if (len <= 0) return;
+  int64_t head, nchunks;
+  bulk_split(p, len, &head, &nchunks);
+  const float* body = p + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    if (r.issued >= BK_STAGES) mbar_wait(&r.empty[r.stage], r.phase ^ 1);
+    mbar_arrive_expect_tx(&r.full[r.stage], BK_CHUNK);
+    void* dst = r.buf + (size_t)r.stage * BK_CHUNK;
+    if (HINT) bulk_g2s_hint(dst, body + c * BK_CF, BK_CHUNK, &r.full[r.stage], pol);
+    else bulk_g2s(dst, body + c * BK_CF, BK_CHUNK, &r.full[r.stage]);
+    ++r.issued;
+    r.advance();
+  }
+}
+
+// Consumer side (warps 1..8, ct = consumer thread index): acc += this CTA's share.
+__device__ __forceinline__ void bulk_consume(BulkRing& r, const float* p, int64_t len, double& acc,
+                                             int ct) {
+  if (len <= 0) return;
+  int64_t head, nchunks;
+  bulk_split(p, len, &head, &nchunks);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
+#pragma unroll
+    for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;  // 8-float group i of the chunk
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+      f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+      acc += sum8(v);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * BK_CF;  // remainder, then the head: plain loads
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    acc += (double)p[i];
+  if (blockIdx.x == 0 && ct < head) acc += (double)p[ct];
+}
+
+__device__ __forceinline__ BulkRing bulk_ring_init(unsigned char* buf, uint64_t* full, uint64_t* empty) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < BK_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -174,42 +230,25 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  return BulkRing{buf, full, empty, 0, 0u, 0};
+}
+
+// Pass 1, TMA-bulk variant for n >= 2^22 (one CTA per SM), then the same
+// last-CTA ticket combine as reduce_kernel.
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                       unsigned* __restrict__ ticket, double* __restrict__ S_out) {
+  pdl_launch_dependents();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ double red[BK_THREADS / 32];
+  __shared__ unsigned is_last;
+  BulkRing r = bulk_ring_init(ring, full, empty);
   double acc = 0.0;
-  if (warp == 0) {
-    if (lane == 0) {  // producer
-      int s = 0, it = 0;
-      unsigned ph = 0;
-      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-        if (it >= BK_STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], BK_CHUNK);
-        bulk_g2s(ring + (size_t)s * BK_CHUNK, body + c * CF, BK_CHUNK, &full[s]);
-        if (++s == BK_STAGES) { s = 0; ph ^= 1; }
-      }
-    }
-  } else {  // consumers
-    const int ct = threadIdx.x - 32;
-    int s = 0;
-    unsigned ph = 0;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      mbar_wait(&full[s], ph);
-      const float4* p = reinterpret_cast<const float4*>(ring + (size_t)s * BK_CHUNK);
-#pragma unroll
-      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
-        const int i = k * BK_CONSUMERS + ct;  // 8-float group i of the chunk
-        const float4 a = p[2 * i], b = p[2 * i + 1];
-        f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
-        acc += sum8(v);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == BK_STAGES) { s = 0; ph ^= 1; }
-    }
-    // remainder after the whole chunks, and the head: plain loads
-    const int64_t rbeg = head + nchunks * CF;
-    for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < n;
-         i += (int64_t)gridDim.x * BK_CONSUMERS)
-      acc += (double)__ldg(in + i);
-    if (blockIdx.x == 0 && ct < head) acc += (double)__ldg(in + ct);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, n, 0);
+  } else {
+    bulk_consume(r, in, n, acc, threadIdx.x - 32);
   }
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
@@ -318,33 +357,42 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
 }
 
-// Single pass over HBM when the covered prefix fits in L2: the uncovered tail is
-// streamed with evict_first, the covered prefix read LAST with evict_last, grid
-// barrier, every CTA combines the partials in the same fixed order, then the
-// prefix is scaled from L2.  Co-residency guaranteed by cooperative launch.
+// Single pass over HBM when the covered prefix fits in L2: one cooperative CTA
+// per SM streams the uncovered tail [L, n) through the TMA-bulk ring with an L2
+// evict_first hint, then the covered prefix [0, L) with evict_last (read LAST,
+// so it is the most recent data in L2); grid barrier; every CTA combines the
+// per-CTA partials in the same fixed order (identical s everywhere); then all
+// threads scale the prefix out of L2.  Co-residency by cooperative launch.
 template <bool VEC>
-__global__ void __launch_bounds__(FU_THREADS, 2)
+__global__ void __launch_bounds__(BK_THREADS, 1)
     fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
                  unsigned* bar, float* sum_out, double* sum_out_f64) {
-  __shared__ double red[FU_THREADS / 32];
-  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ double red[BK_THREADS / 32];
+  BulkRing r = bulk_ring_init(ring, full, empty);
   double acc = 0.0;
-  // LD_HINT loads are coherent (no .nc): `out` may alias `in` in phase 2.
-  accumulate_segment<FU_THREADS, FU_UNROLL, LD_HINT>(in + L, n - L, blockIdx.x, gridDim.x, acc,
-                                                     pol_first);
-  accumulate_segment<FU_THREADS, FU_UNROLL, LD_HINT>(in, L, blockIdx.x, gridDim.x, acc, pol_last);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      bulk_produce<true>(r, in + L, n - L, policy_evict_first());
+      bulk_produce<true>(r, in, L, policy_evict_last());
+    }
+  } else {
+    bulk_consume(r, in + L, n - L, acc, threadIdx.x - 32);
+    bulk_consume(r, in, L, acc, threadIdx.x - 32);
+  }
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
-  grid_barrier(bar);
+  grid_barrier(bar);  // all of `in` has been read: `out` (possibly == in) may be written
   double v = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += FU_THREADS) v += __ldcg(partials + i);
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
   const double S = block_sum(v, red);  // identical bits in every CTA
   const float s = (float)S;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (sum_out) *sum_out = s;
     if (sum_out_f64) *sum_out_f64 = S;
   }
-  scale_segment<FU_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
+  scale_segment<BK_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
 }
 
 // ----------------------------------------------------------------- rows
@@ -455,7 +503,7 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
                           const DeviceInfo& d, cudaStream_t st) {
   if (n >= kBulkMinN) {
     static int configured[64] = {0};  // per device: opt in to 128 KiB of dynamic smem
-    const size_t smem = (size_t)BK_STAGES * BK_CHUNK;
+    const size_t smem = BK_SMEM;
     if (d.device < 64 && !configured[d.device]) {
       cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
@@ -527,18 +575,22 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
                          cudaStream_t st) {
   const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
   void* fn = vec ? (void*)fused_kernel<true> : (void*)fused_kernel<false>;
+  static int configured[64][2] = {};
+  if (d.device < 64 && !configured[d.device][vec]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM);
+    if (e != cudaSuccess) return e;
+    configured[d.device][vec] = 1;
+  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, FU_THREADS, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BK_THREADS, BK_SMEM);
   if (e != cudaSuccess) return e;
-  if (per_sm > 2) per_sm = 2;
   if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-  int grid = d.sms * per_sm;
-  if (grid > kMaxGrid) grid = kMaxGrid;
+  int grid = d.sms;  // one CTA per SM
   int64_t n = cov.n, L = cov.L;
   double* partials = ws.partials;
   unsigned* bar = ws.bar;
   void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64};
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FU_THREADS), args, 0, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BK_THREADS), args, BK_SMEM, st);
 }
 
 cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,

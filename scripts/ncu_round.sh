@@ -15,9 +15,9 @@ ncu --set full --clock-control none --import-source on -k regex:scale_kernel -s 
     -o $OUT/${TAG}_scale python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 3 -c 1 \
     -o $OUT/${TAG}_fused python bench.py --workload paths28 --steps 3 --warmup 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:rows_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:rows_vec_kernel -s 3 -c 1 \
     -o $OUT/${TAG}_rows_dense python bench.py --workload rows --index dense --steps 3 --warmup 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:rows_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:rows_vec_kernel -s 3 -c 1 \
     -o $OUT/${TAG}_rows_literal python bench.py --workload rows --index literal --steps 3 --warmup 3 > /dev/null 2>&1
 ls -la $OUT
 ncu --set full --clock-control none --import-source on -k regex:softmax_vec -s 3 -c 1 \
