@@ -8,6 +8,8 @@
 // combines (bitwise deterministic), and PDL between the reduce and the scale.
 // DESIGN.md §4 gives each kernel's roofline and algorithmic bytes.
 #include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "device_common.cuh"
 #include "norm_internal.h"
@@ -112,14 +114,15 @@ __device__ __forceinline__ void scale_segment(float* out, const float* in, int64
 // per-CTA partial, last-CTA ticket combines the partials in index order.
 __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
     reduce_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
-                  unsigned* __restrict__ ticket, double* __restrict__ S_out) {
-  // The scale kernel (PDL dependent) may be scheduled as soon as SM resources
-  // free up; it blocks in griddepcontrol.wait until this grid has completed.
-  pdl_launch_dependents();
+                  unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger) {
+  // The scale kernel (PDL dependent) may be scheduled once every CTA has
+  // triggered; it blocks in griddepcontrol.wait until this grid has completed.
+  if (early_trigger) pdl_launch_dependents();
   __shared__ double red[RED_THREADS / 32];
   __shared__ unsigned is_last;
   double acc = 0.0;
   accumulate_segment<RED_THREADS, RED_UNROLL, LD_STREAM>(in, n, blockIdx.x, gridDim.x, acc, 0);
+  if (!early_trigger) pdl_launch_dependents();
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = b;
@@ -147,13 +150,22 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
 // release the stage.  Chunks are dealt grid-strided; the < 32 KiB remainder and
 // the < 16 B head of each segment go through plain loads.  The ring state
 // carries across segments, so a kernel can stream several segments in a row.
-constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32, BK_STAGES = 4;
-constexpr int BK_CHUNK = 32768;        // bytes per stage
-constexpr int64_t BK_CF = BK_CHUNK / 4;  // floats per stage
+constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32;
+constexpr int BK_STAGES = 4, BK_CHUNK = 32768;  // reduce: 4 x 32 KiB in flight per SM
+constexpr int SB_STAGES = 2, SB_CHUNK = 49152;  // scale: 2 x 48 KiB (loads share HBM with stores)
 constexpr size_t BK_SMEM = (size_t)BK_STAGES * BK_CHUNK;
-constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernel is as fast
+// The scale ring uses 96 KiB but reserves 116 KiB (> half of the SM's 228 KiB):
+// exactly one scale CTA fits per SM, so its persistent grid spreads one CTA per
+// SM even when PDL launches it while reduce CTAs are still resident (without
+// the reservation two scale CTAs can land on one SM: measured 0.5 ms slower on
+// dense 2^32).
+constexpr size_t SB_SMEM = 116 * 1024;
+static_assert((size_t)SB_STAGES * SB_CHUNK <= SB_SMEM, "ring fits the reservation");
+constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernels are as fast
 
+template <int STAGES, int CHUNK>
 struct BulkRing {
+  static constexpr int64_t CF = CHUNK / 4;  // floats per stage
   unsigned char* buf;
   uint64_t* full;
   uint64_t* empty;
@@ -161,50 +173,57 @@ struct BulkRing {
   unsigned phase;
   int issued;
   __device__ __forceinline__ void advance() {
-    if (++stage == BK_STAGES) {
+    if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
     }
   }
 };
 
+// head = floats before the first 32-byte boundary of p; then whole chunks.
+template <int64_t CF>
 __device__ __forceinline__ void bulk_split(const float* p, int64_t len, int64_t* head, int64_t* nchunks) {
-  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 15u);
-  int64_t h = (int64_t)(((16u - mis) & 15u) >> 2);
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 31u);
+  int64_t h = (int64_t)(((32u - mis) & 31u) >> 2);
   if (h > len) h = len;
   *head = h;
-  *nchunks = (len - h) / BK_CF;
+  *nchunks = (len - h) / CF;
 }
 
 // Producer side (call from one lane): issue this CTA's chunks of [p, p + len).
-template <bool HINT>
-__device__ __forceinline__ void bulk_produce(BulkRing& r, const float* p, int64_t len, uint64_t pol) {
+template <bool HINT, int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_produce(BulkRing<STAGES, CHUNK>& r, const float* p, int64_t len,
+                                             uint64_t pol) {
   if (len <= 0) return;
+  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
   int64_t head, nchunks;
-  bulk_split(p, len, &head, &nchunks);
+  bulk_split<CF>(p, len, &head, &nchunks);
   const float* body = p + head;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    if (r.issued >= BK_STAGES) mbar_wait(&r.empty[r.stage], r.phase ^ 1);
-    mbar_arrive_expect_tx(&r.full[r.stage], BK_CHUNK);
-    void* dst = r.buf + (size_t)r.stage * BK_CHUNK;
-    if (HINT) bulk_g2s_hint(dst, body + c * BK_CF, BK_CHUNK, &r.full[r.stage], pol);
-    else bulk_g2s(dst, body + c * BK_CF, BK_CHUNK, &r.full[r.stage]);
+    if (r.issued >= STAGES) mbar_wait(&r.empty[r.stage], r.phase ^ 1);
+    mbar_arrive_expect_tx(&r.full[r.stage], CHUNK);
+    void* dst = r.buf + (size_t)r.stage * CHUNK;
+    if (HINT) bulk_g2s_hint(dst, body + c * CF, CHUNK, &r.full[r.stage], pol);
+    else bulk_g2s(dst, body + c * CF, CHUNK, &r.full[r.stage]);
     ++r.issued;
     r.advance();
   }
 }
 
 // Consumer side (warps 1..8, ct = consumer thread index): acc += this CTA's share.
-__device__ __forceinline__ void bulk_consume(BulkRing& r, const float* p, int64_t len, double& acc,
-                                             int ct) {
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_consume(BulkRing<STAGES, CHUNK>& r, const float* p, int64_t len,
+                                             double& acc, int ct) {
   if (len <= 0) return;
+  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
+  static_assert(CHUNK % (32 * BK_CONSUMERS) == 0, "whole 8-float groups per consumer");
   int64_t head, nchunks;
-  bulk_split(p, len, &head, &nchunks);
+  bulk_split<CF>(p, len, &head, &nchunks);
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     mbar_wait(&r.full[r.stage], r.phase);
-    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * CHUNK);
 #pragma unroll
-    for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+    for (int k = 0; k < CHUNK / 32 / BK_CONSUMERS; ++k) {
       const int i = k * BK_CONSUMERS + ct;  // 8-float group i of the chunk
       const float4 a = q[2 * i], b = q[2 * i + 1];
       f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
@@ -214,42 +233,45 @@ __device__ __forceinline__ void bulk_consume(BulkRing& r, const float* p, int64_
     if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[r.stage]);
     r.advance();
   }
-  const int64_t rbeg = head + nchunks * BK_CF;  // remainder, then the head: plain loads
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head: plain loads
   for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
        i += (int64_t)gridDim.x * BK_CONSUMERS)
     acc += (double)p[i];
   if (blockIdx.x == 0 && ct < head) acc += (double)p[ct];
 }
 
-__device__ __forceinline__ BulkRing bulk_ring_init(unsigned char* buf, uint64_t* full, uint64_t* empty) {
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char* buf, uint64_t* full,
+                                                                  uint64_t* empty) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < BK_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], BK_CONSUMERS / 32);
     }
     mbar_fence_init();
   }
   __syncthreads();
-  return BulkRing{buf, full, empty, 0, 0u, 0};
+  return BulkRing<STAGES, CHUNK>{buf, full, empty, 0, 0u, 0};
 }
 
 // Pass 1, TMA-bulk variant for n >= 2^22 (one CTA per SM), then the same
 // last-CTA ticket combine as reduce_kernel.
 __global__ void __launch_bounds__(BK_THREADS, 1)
     reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
-                       unsigned* __restrict__ ticket, double* __restrict__ S_out) {
-  pdl_launch_dependents();
+                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger) {
+  if (early_trigger) pdl_launch_dependents();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
   __shared__ double red[BK_THREADS / 32];
   __shared__ unsigned is_last;
-  BulkRing r = bulk_ring_init(ring, full, empty);
+  auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   double acc = 0.0;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) bulk_produce<false>(r, in, n, 0);
   } else {
     bulk_consume(r, in, n, acc, threadIdx.x - 32);
   }
+  if (!early_trigger) pdl_launch_dependents();
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = b;
@@ -293,6 +315,63 @@ __global__ void __launch_bounds__(SC_THREADS)
   }
   __syncthreads();
   scale_segment<SC_THREADS, SC_UNROLL, VEC, ALIAS>(out, in, len, s_sh, blockIdx.x, gridDim.x);
+}
+
+// Scale, TMA-bulk variant for len >= 2^22 with out/in co-aligned mod 32 B: one
+// CTA per SM, 2 x 48 KiB chunks of `in` in flight per SM via cp.async.bulk
+// (the measured optimum for a read+write stream: 6.76 TB/s vs 6.12 TB/s for
+// LDG/STG and 6.57 TB/s for cudaMemcpy D2D, scripts/microbench_scale.cu);
+// consumers divide out of shared memory and store with STG.E.256 (.cs).  The
+// producer starts streaming BEFORE griddepcontrol.wait — `in` is not written by
+// the preceding reduce — so under PDL the first chunks overlap the reduce's
+// tail; no store happens before the wait (out may alias in).
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    scale_bulk_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
+                      int nparts, float* sum_out, double* sum_out_f64) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[SB_STAGES], empty[SB_STAGES];
+  __shared__ float s_sh;
+  auto r = bulk_ring_init<SB_STAGES, SB_CHUNK>(ring, full, empty);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, len, 0);
+    return;
+  }
+  const int ct = threadIdx.x - 32;
+  pdl_wait();
+  if (ct == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
+  const float s = s_sh, rs = __frcp_rn(s);
+  constexpr int64_t CF = SB_CHUNK / 4;
+  int64_t head, nchunks;
+  bulk_split<CF>(in, len, &head, &nchunks);
+  float* ob = out + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * SB_CHUNK);
+    float* oc = ob + c * CF;
+#pragma unroll
+    for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, s, rs));
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    out[i] = div_rn(in[i], s, rs);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], s, rs);
 }
 
 __global__ void __launch_bounds__(256)
@@ -370,7 +449,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
   __shared__ double red[BK_THREADS / 32];
-  BulkRing r = bulk_ring_init(ring, full, empty);
+  auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   double acc = 0.0;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
@@ -499,6 +578,19 @@ int reduce_grid(const DeviceInfo& d, int64_t n) {
   return (int)g;
 }
 
+// Programmatic dependent launch of the scale after the reduce.  NORM_PDL=off |
+// early (trigger at the reduce's start) | late (trigger after its streaming loop,
+// the default): a tuning knob read once; every mode gives identical results.
+int pdl_mode() {
+  static int mode = [] {
+    const char* e = getenv("NORM_PDL");
+    if (e && !strcmp(e, "off")) return (int)PDL_OFF;
+    if (e && !strcmp(e, "early")) return (int)PDL_EARLY;
+    return (int)PDL_LATE;
+  }();
+  return mode;
+}
+
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
                           const DeviceInfo& d, cudaStream_t st) {
   if (n >= kBulkMinN) {
@@ -510,11 +602,29 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
       if (e != cudaSuccess) return e;
       configured[d.device] = 1;
     }
-    reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out);
+    reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
+                                                        pdl_mode() == PDL_EARLY);
     return cudaGetLastError();
   }
-  reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out);
+  reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out,
+                                                            pdl_mode() == PDL_EARLY);
   return cudaGetLastError();
+}
+
+template <typename Kern, typename... Args>
+static cudaError_t launch_maybe_pdl_smem(Kern k, int grid, int block, size_t smem, bool pdl,
+                                         cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_mode() != PDL_OFF) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 template <typename Kern, typename... Args>
@@ -529,7 +639,7 @@ static cudaError_t launch_maybe_pdl(Kern k, int grid, int block, bool pdl, cudaS
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (pdl && pdl_mode() != PDL_OFF) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -543,6 +653,17 @@ cudaError_t launch_scale(float* out, const float* in, int64_t len, const double*
   if (g < 1) g = 1;
   const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
   const bool alias = out == in;
+  if (vec && len >= kBulkMinN) {
+    static int configured[64] = {0};
+    if (d.device < 64 && !configured[d.device]) {
+      cudaError_t e = cudaFuncSetAttribute(scale_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)SB_SMEM);
+      if (e != cudaSuccess) return e;
+      configured[d.device] = 1;
+    }
+    return launch_maybe_pdl_smem(scale_bulk_kernel, d.sms, BK_THREADS, SB_SMEM, pdl, st, out, in,
+                                 len, S_parts, nparts, sum_out, sum_out_f64);
+  }
   if (vec && alias)
     return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
                             S_parts, nparts, sum_out, sum_out_f64);

@@ -45,6 +45,9 @@ struct DeviceInfo {
 // Cached per device; returns false (with detail) if the device is unusable.
 bool device_info(DeviceInfo* out, std::string* err);
 
+enum PdlMode { PDL_OFF = 0, PDL_EARLY = 1, PDL_LATE = 2 };
+int pdl_mode();  // NORM_PDL env knob, read once (kernels.cu)
+
 // ---- kernel launchers (kernels.cu).  All return the launch's cudaError_t. ----
 // Tuning constants live next to the kernels.
 int reduce_grid(const DeviceInfo& d, int64_t n);

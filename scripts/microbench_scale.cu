@@ -5,6 +5,7 @@
 //        -I paper_2207_00257_b200/csrc scripts/microbench_scale.cu -o scripts/mb_scale
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "device_common.cuh"
 
@@ -94,6 +95,65 @@ __global__ void __launch_bounds__(NC + 32, 1) sc_bulk(float* out, const float* i
   }
 }
 
+// bulk load -> divide in shared memory -> bulk store (TMA both ways).  Each stage:
+// full[s] (TMA load landed) -> consumers transform in place -> bar.sync among
+// consumers -> one consumer thread issues cp.async.bulk.global.shared::cta store,
+// commits, waits until the store has READ the smem (wait_group.read) -> empty[s].
+template <int NC, int ST, int CB>
+__global__ void __launch_bounds__(NC + 32, 1) sc_bulk2(float* out, const float* in, int64_t n, float s) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int64_t CF = CB / 4;
+  const int64_t nchunks = n / CF;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0, it = 0;
+      unsigned ph = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        if (it >= ST) mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], CB);
+        bulk_g2s(ring + (size_t)st * CB, in + c * CF, CB, &full[st]);
+        if (++st == ST) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    const int ct = threadIdx.x - 32;
+    const float rs = __frcp_rn(s);
+    int st = 0;
+    unsigned ph = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      mbar_wait(&full[st], ph);
+      float4* p = reinterpret_cast<float4*>(ring + (size_t)st * CB);
+#pragma unroll 4
+      for (int i = ct; i < CB / 16; i += NC) {
+        float4 a = p[i];
+        a.x = div_rn(a.x, s, rs); a.y = div_rn(a.y, s, rs); a.z = div_rn(a.z, s, rs); a.w = div_rn(a.w, s, rs);
+        p[i] = a;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+      asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+      if (ct == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + c * CF),
+                     "r"(smem_addr(p)), "r"(CB) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&empty[st]);
+      }
+      if (++st == ST) { st = 0; ph ^= 1; }
+    }
+    if (ct == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -114,14 +174,23 @@ float timeit(F f) {
   return best;
 }
 
-int main() {
-  const int64_t n = 1ll << 31;  // 8 GiB in, 8 GiB out
+__global__ void fill_hash(float* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)(i * 2654435761u) ^ (uint32_t)(i >> 7);
+    p[i] = 0.5f + (float)(h >> 8) * 5.9604645e-08f;
+  }
+}
+
+int main(int argc, char** argv) {
+  const int64_t n = 1ll << (argc > 1 ? atoi(argv[1]) : 31);  // default 8 GiB in, 8 GiB out
+  const bool random = argc > 2;
   float *in, *out;
   if (cudaMalloc(&in, n * 4) != cudaSuccess || cudaMalloc(&out, n * 4) != cudaSuccess) {
     printf("alloc failed\n");
     return 1;
   }
   cudaMemset(in, 0x3F, n * 4);  // 0x3F3F3F3F = 0.747f (zeros take __fdiv_rn's slow path)
+  if (random) fill_hash<<<148 * 8, 256>>>(in, n);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double bytes = 8.0 * n;
@@ -152,6 +221,24 @@ int main() {
   RUNB("bulk-load 512c 4x32KiB + stg.cs", 512, 4, 32768);
   RUNB("bulk-load 256c 3x32KiB + stg.cs", 256, 3, 32768);
   RUNB("bulk-load 256c 6x32KiB + stg.cs", 256, 6, 32768);
+#define RUNB2(NAME, NC, ST, CB)                                                                  \
+  {                                                                                             \
+    cudaFuncSetAttribute(sc_bulk2<NC, ST, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CB); \
+    float ms = timeit([&] { sc_bulk2<NC, ST, CB><<<sms, NC + 32, ST * CB>>>(out, in, n, s); });   \
+    printf("%-42s %8.3f ms %8.1f GB/s %s\n", NAME, ms, bytes / ms / 1e6,                        \
+           cudaGetErrorString(cudaGetLastError()));                                             \
+  }
+  static_assert(true, "");
+  RUNB("bulk-load 256c 2x40KiB + stg.cs", 256, 2, 40960);
+  RUNB("bulk-load 256c 2x48KiB + stg.cs", 256, 2, 49152);
+  RUNB("bulk-load 256c 2x56KiB + stg.cs", 256, 2, 57344);
+  RUNB("bulk-load 256c 2x64KiB + stg.cs", 256, 2, 65536);
+  RUNB("bulk-load 256c 3x40KiB + stg.cs", 256, 3, 40960);
+  RUNB("bulk-load 256c 3x48KiB + stg.cs", 256, 3, 49152);
+  RUNB("bulk-load 256c 4x24KiB + stg.cs", 256, 4, 24576);
+  RUNB("bulk-load 512c 2x48KiB + stg.cs", 512, 2, 49152);
+  RUNB("bulk-load 128c 2x48KiB + stg.cs", 128, 2, 49152);
+  RUNB("bulk-load 256c 6x16KiB + stg.cs", 256, 6, 16384);
   cudaMemset(in, 0, n * 4);  // all-zero dividends: must not fall to the slow path
   RUN("ldg/stg.cs 256x4 U4, zero input", (sc_ldg<256, 4, 4>), 256, 4);
   cudaMemset(in, 0x3F, n * 4);
