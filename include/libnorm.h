@@ -75,10 +75,11 @@ typedef enum {
 } norm_index_t;
 
 typedef enum {
-  NORM_PATH_AUTO = 0,     /* small: one CTA; covered bytes fit L2: fused; else two-pass   */
+  NORM_PATH_AUTO = 0,     /* n <= 2^17: small; input > L2 but covered prefix fits: fused;
+                             else two-pass                                 */
   NORM_PATH_TWO_PASS = 1, /* reduce kernel, then scale kernel (PDL-chained)               */
   NORM_PATH_FUSED = 2,    /* one cooperative kernel: reduce, grid barrier, scale from L2  */
-  NORM_PATH_SMALL = 3     /* one CTA does everything (any n; intended for n <= 2^15)       */
+  NORM_PATH_SMALL = 3     /* one CTA does everything (any n; intended for n <= 2^17)       */
 } norm_path_t;
 
 typedef struct {

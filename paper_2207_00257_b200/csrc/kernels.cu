@@ -547,6 +547,89 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
   }
 }
 
+// Batched rows, TMA-staged, one WARP per row (rows of <= 48 KiB, 16-byte aligned
+// with cols % 4 == 0).  One CTA per SM: lane 0 of warp 0 streams whole rows
+// into a ring of S = 2W shared-memory stages with cp.async.bulk; consumer warp w
+// owns stages w and w + W and processes this CTA's rows k = w, w + W, ...: sum
+// the row out of shared memory, warp-shuffle reduce (no block barrier on the
+// per-row critical path), then scale the covered elements out of shared memory
+// into `out`.  Up to S rows are in flight per SM, so HBM stays busy while each
+// warp finishes its row.
+constexpr int RB_MAX_STAGES = 16;
+constexpr size_t RB_SMEM_BUDGET = 200 * 1024;
+
+__global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
+    rows_bulk_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
+                     int64_t ld_in, int64_t L, int64_t G, int S, float* sum_out,
+                     double* sum_out_f64) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[RB_MAX_STAGES], empty[RB_MAX_STAGES];
+  const int W = S / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned row_bytes = (unsigned)(cols * 4);
+  const size_t stage_bytes = ((size_t)row_bytes + 127) & ~(size_t)127;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t step = gridDim.x;
+  if (warp == 0) {
+    if (lane == 0) {
+      int64_t k = 0;
+      for (int64_t r = blockIdx.x; r < rows; r += step, ++k) {
+        const int st = (int)(k % S);
+        if (k >= S) mbar_wait(&empty[st], (unsigned)(((k / S) - 1) & 1));
+        mbar_arrive_expect_tx(&full[st], row_bytes);
+        bulk_g2s(ring + st * stage_bytes, in + r * ld_in, row_bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  const int w = warp - 1;
+  const int nq = (int)(cols >> 2);  // float4s per row
+  const bool vst = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (ld_out % 4 == 0);
+  for (int64_t k = w; blockIdx.x + k * step < rows; k += W) {
+    const int64_t r = blockIdx.x + k * step;
+    const int st = (int)(k % S);
+    mbar_wait(&full[st], (unsigned)((k / S) & 1));
+    const float4* q = reinterpret_cast<const float4*>(ring + st * stage_bytes);
+    double acc = 0.0;
+    for (int j = lane; j < nq; j += 32) {
+      const float4 a = q[j];
+      acc += (double)((a.x + a.y) + (a.z + a.w));
+    }
+    const double Srow = warp_sum(acc);
+    const float s = (float)Srow, rs = __frcp_rn(s);
+    if (lane == 0) {
+      if (sum_out) sum_out[r] = s;
+      if (sum_out_f64) sum_out_f64[r] = Srow;
+    }
+    float* dst = out + r * ld_out;
+    const float* src = reinterpret_cast<const float*>(q);
+    if (L >= 0) {
+      const int full4 = (int)(L >> 2);
+      for (int j = lane; j < full4; j += 32) {
+        const float4 a = q[j];
+        const float4 y = make_float4(div_rn(a.x, s, rs), div_rn(a.y, s, rs), div_rn(a.z, s, rs),
+                                     div_rn(a.w, s, rs));
+        if (vst) __stcs(reinterpret_cast<float4*>(dst) + j, y);
+        else { dst[4 * j] = y.x; dst[4 * j + 1] = y.y; dst[4 * j + 2] = y.z; dst[4 * j + 3] = y.w; }
+      }
+      const int64_t t = (int64_t)full4 * 4 + lane;
+      if (lane < 4 && t < L) dst[t] = div_rn(src[t], s, rs);
+    } else {
+      for (int64_t i = lane; i < cols; i += 32)
+        if ((i % 32) < G) dst[i] = div_rn(src[i], s, rs);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
 // Any shape / alignment: one CTA per row, a scalar sum sweep then a scale sweep.
 __global__ void __launch_bounds__(ROW_THREADS)
     rows_generic_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
@@ -725,6 +808,34 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
                        (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
   const bool vec = aligned && cols <= (int64_t)ROW_THREADS * 8 * ROW_MAXV;
   const bool alias = out == in;
+  // The warp-per-row TMA kernel wins when few elements are written (literal rows:
+  // 6.1 vs 5.4 TB/s at 65536x4096); with every element written the per-warp
+  // division/store work needs more warps than it has, and the register-resident
+  // CTA-per-row kernel wins (5.9 vs 4.5 TB/s, dense) -- DESIGN.md §4.
+  const int64_t covered = rc.kind == COV_PREFIX ? rc.L : rc.count;
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) && (ld_in % 4) == 0 &&
+                       (cols % 4) == 0 && cols * 4 <= 48 * 1024 && cols >= 256 &&
+                       covered * 2 <= cols;
+  if (bulk_ok && !getenv("NORM_ROWS_NO_BULK")) {
+    const size_t stage_bytes = ((size_t)cols * 4 + 127) & ~(size_t)127;
+    int S = (int)(RB_SMEM_BUDGET / stage_bytes);
+    if (S > RB_MAX_STAGES) S = RB_MAX_STAGES;
+    S &= ~1;
+    if (S >= 2) {
+      static int configured[64] = {0};
+      if (d.device < 64 && !configured[d.device]) {
+        cudaError_t e = cudaFuncSetAttribute(rows_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)RB_SMEM_BUDGET);
+        if (e != cudaSuccess) return e;
+        configured[d.device] = 1;
+      }
+      int64_t gb = d.sms;
+      if (rows < gb) gb = rows;
+      rows_bulk_kernel<<<(int)gb, 32 * (1 + S / 2), (size_t)S * stage_bytes, st>>>(
+          out, in, rows, cols, ld_out, ld_in, L, rc.G, S, sum_out, sum_out_f64);
+      return cudaGetLastError();
+    }
+  }
 #define NORM_ROWS(A, M)                                                                           \
   rows_vec_kernel<A, M><<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, rc.G, \
                                                        sum_out, sum_out_f64)

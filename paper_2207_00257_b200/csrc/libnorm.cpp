@@ -210,14 +210,22 @@ static norm_status_t check_literal_grid(const Coverage& c, int index) {
   return NORM_OK;
 }
 
-// AUTO path thresholds: tuned on B200.
-constexpr int64_t kSmallN = 16384;
+// AUTO path thresholds, measured on B200 (scripts/small_paths.py,
+// bench.py --workload paths28):
+//  * n <= 2^17: one CTA does everything (3-6 us; the two-kernel path costs ~6.5 us);
+//  * fused only pays when the input does NOT fit in L2 but the covered prefix
+//    does: then the scale reads the prefix from L2 instead of HBM (literal 2^28:
+//    0.180 vs 0.187 ms).  When the whole input fits in L2 the two-pass scale hits
+//    L2 anyway and the cooperative launch + grid barrier only cost (~1 us);
+//  * otherwise two-pass.
+constexpr int64_t kSmallN = 1 << 17;
 
 static int choose_path(const Coverage& cov, const norm_opts_t* o, const DeviceInfo& d) {
   if (o->path != NORM_PATH_AUTO) return o->path;
   if (cov.n <= kSmallN) return NORM_PATH_SMALL;
   const size_t budget = d.l2_bytes / 3;  // covered bytes kept in L2 across the grid barrier
-  if (cov.kind == COV_PREFIX && (size_t)cov.L * 4 <= budget) return NORM_PATH_FUSED;
+  if (cov.kind == COV_PREFIX && (size_t)cov.n * 4 > d.l2_bytes && (size_t)cov.L * 4 <= budget)
+    return NORM_PATH_FUSED;
   return NORM_PATH_TWO_PASS;
 }
 

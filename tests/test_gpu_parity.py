@@ -189,8 +189,12 @@ def test_large_sampled_2_28():
 
 @pytest.mark.parametrize("mode", ["literal", "dense"])
 def test_rows_parity(mode):
+    # kernel coverage: 65536x4096 / 5x10000 / 1x8192 literal -> TMA warp-per-row kernel
+    # (9x512 literal: residue coverage there); dense and other shapes -> register-
+    # resident CTA-per-row kernel; 4099 / 703 / 72 -> generic kernel
     shapes = [(65536, 4096, 4096), (7, 1000, 1000), (3, 4099, 4100), (5, 10000, 10000),
-              (33, 64, 72), (4, 700, 703), (1, 8192, 8192), (2, 1, 1)]
+              (33, 64, 72), (4, 700, 703), (1, 8192, 8192), (2, 1, 1), (9, 512, 512),
+              (300, 2048, 2056)]
     for i, (R, C, ld) in enumerate(shapes):
         d = DISTS[i % 5]
         x = np.zeros((R, ld), np.float32)
@@ -212,16 +216,17 @@ def test_rows_parity(mode):
             assert np.all(o[:, :C][:, ~cov].view(np.uint32) == SENTINEL_BITS)
 
 
-def test_rows_deterministic_and_in_place():
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_rows_deterministic_and_in_place(mode):
     R, C = 1000, 4096
     x = gen.make_host(R * C, seed=5, dist=4).reshape(R, C)
     a = to_dev(x)
-    o1 = torch.empty_like(a)
-    o2 = torch.empty_like(a)
-    L.normalize_rows(o1, a, index="dense")
-    L.normalize_rows(o2, a, index="dense")
+    o1 = a.clone()
+    o2 = a.clone()
+    L.normalize_rows(o1, a, index=mode)
+    L.normalize_rows(o2, a, index=mode)
     b = a.clone()
-    L.normalize_rows(b, b, index="dense")
+    L.normalize_rows(b, b, index=mode)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(o1, b)
 
