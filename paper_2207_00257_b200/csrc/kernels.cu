@@ -21,7 +21,7 @@ constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
 constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
 constexpr int SMALL_THREADS = 1024;
 constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 4;
-constexpr int FU_SCALE_UNROLL = 2;
+constexpr int FU_SCALE_UNROLL = 8;  // fused phase 2 reads from L2: 256 B in flight per thread
 
 enum LoadKind { LD_STREAM = 0, LD_HINT = 1, LD_PLAIN = 2 };
 
@@ -200,7 +200,7 @@ __device__ __forceinline__ void bulk_produce(BulkRing<STAGES, CHUNK>& r, const f
   bulk_split<CF>(p, len, &head, &nchunks);
   const float* body = p + head;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    if (r.issued >= STAGES) mbar_wait(&r.empty[r.stage], r.phase ^ 1);
+    if (r.issued >= STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
     mbar_arrive_expect_tx(&r.full[r.stage], CHUNK);
     void* dst = r.buf + (size_t)r.stage * CHUNK;
     if (HINT) bulk_g2s_hint(dst, body + c * CF, CHUNK, &r.full[r.stage], pol);
@@ -229,8 +229,7 @@ __device__ __forceinline__ void bulk_consume(BulkRing<STAGES, CHUNK>& r, const f
       f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
       acc += sum8(v);
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[r.stage]);
+    stage_release(&r.empty[r.stage]);
     r.advance();
   }
   const int64_t rbeg = head + nchunks * CF;  // remainder, then the head: plain loads
@@ -363,8 +362,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
       const float4 a = q[2 * i], b = q[2 * i + 1];
       st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, s, rs));
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[r.stage]);
+    stage_release(&r.empty[r.stage]);
     r.advance();
   }
   const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
@@ -582,7 +580,7 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
       int64_t k = 0;
       for (int64_t r = blockIdx.x; r < rows; r += step, ++k) {
         const int st = (int)(k % S);
-        if (k >= S) mbar_wait(&empty[st], (unsigned)(((k / S) - 1) & 1));
+        if (k >= S) stage_acquire(&empty[st], (unsigned)(((k / S) - 1) & 1));
         mbar_arrive_expect_tx(&full[st], row_bytes);
         bulk_g2s(ring + st * stage_bytes, in + r * ld_in, row_bytes, &full[st]);
       }
@@ -625,8 +623,7 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
       for (int64_t i = lane; i < cols; i += 32)
         if ((i % 32) < G) dst[i] = div_rn(src[i], s, rs);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    stage_release(&empty[st]);
   }
 }
 

@@ -467,3 +467,44 @@ def test_signed_zeros_and_zero_heavy():
                     out, s, _ = run(xs, mode, path)
                     rep = oracle.replay(xs, s, mode, out=sentinel(n))
                     assert out.view(np.uint32).tobytes() == rep.view(np.uint32).tobytes()
+
+
+def test_bulk_ring_stage_reuse_stress():
+    """The TMA-bulk rings (reduce 4 x 32 KiB, scale 2 x 48 KiB, rows) reuse each
+    shared-memory stage many times per CTA.  Every 32 KiB chunk here carries a
+    different integer value, so a stage refilled before its consumers finished
+    (a missing release/acquire) would change the sum or the outputs; the exact
+    sum is an integer, exactly representable, and must come out exactly, 20
+    runs in a row.  (compute-sanitizer racecheck flags this mbarrier-ordered
+    WAR pattern; see profiles/sanitize_r03.md.)"""
+    n = 2**26 + 5
+    chunk = 8192
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    x = ((idx // chunk) % 97 + 1).to(torch.float32)
+    exact = float(((torch.arange(n, dtype=torch.int64) // chunk) % 97 + 1).sum().item())
+    out = torch.empty_like(x)
+    S = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s = torch.zeros(1, device="cuda")
+    first = None
+    for _ in range(20):
+        L.normalize(out, x, index="dense", path="two_pass", sum_out=s, sum_out_f64=S)
+        torch.cuda.synchronize()
+        assert S.item() == exact
+        if first is None:
+            first = out.clone()
+            xs = x[:: 4099].cpu().numpy()
+            assert np.array_equal(out[:: 4099].cpu().numpy(), xs / np.float32(s.item()))
+        else:
+            assert torch.equal(out, first)
+    for _ in range(5):
+        L.normalize(out, x, index="literal", path="fused", sum_out_f64=S)
+        torch.cuda.synchronize()
+        assert S.item() == exact
+    R, C = 4096, 4096
+    m = ((torch.arange(R * C, device="cuda") // C) % 89 + 1).to(torch.float32).view(R, C)
+    o = torch.zeros_like(m)
+    sr = torch.zeros(R, dtype=torch.float64, device="cuda")
+    L.normalize_rows(o, m, index="literal", sum_out_f64=sr)
+    torch.cuda.synchronize()
+    expect = ((torch.arange(R, device="cuda") % 89 + 1) * C).double()
+    assert torch.equal(sr, expect)
