@@ -50,6 +50,7 @@ def lib():
         L.oracle_nll_forward.argtypes = [vp, dp, vp, vp, vp, i64, i64, i64, ctypes.c_int, i64]
         L.oracle_nll_backward.argtypes = [vp, vp, vp, vp, ctypes.c_double, i64, i64, i64,
                                           ctypes.c_int, i64]
+        L.oracle_bpnn_layerforward.argtypes = [vp, vp, vp, i64, i64]
         _lib = L
     return _lib
 
@@ -200,3 +201,19 @@ def nll_backward(grad_out, target, C, weight=None, reduction="mean", ignore_inde
                                    N, C, C, RED[reduction], ignore_index)
     assert rc == 0
     return grad
+
+
+# ------------------------------------------------ NEXT-4: backprop layerforward
+
+def bpnn_layerforward(input_units, hidden_weights, hid=16):
+    """Rodinia bpnn_layerforward (Fig. backprop) step by step in fp32.
+    input_units: fp32[in + 1]; hidden_weights: fp32[(in + 1), hid + 1] (not modified).
+    Returns (hidden_after, output[in])."""
+    inp = np.ascontiguousarray(input_units, dtype=np.float32)
+    hw = np.array(hidden_weights, dtype=np.float32, copy=True, order="C")
+    n_in = inp.size - 1
+    out = np.zeros(max(n_in, 1), dtype=np.float32)
+    rc = lib().oracle_bpnn_layerforward(inp.ctypes.data, hw.ctypes.data, out.ctypes.data, n_in, hid)
+    if rc:
+        raise ValueError("bad backprop arguments (hid == 16, in % 16 == 0)")
+    return hw, out[:n_in]

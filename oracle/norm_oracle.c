@@ -342,3 +342,38 @@ int oracle_nll_backward(double* grad, const double* grad_out, const int64_t* tar
   }
   return 0;
 }
+
+/* ================================================================ NEXT-4
+ * bpnn_layerforward of Rodinia backprop as printed in Fig. backprop
+ * (PAPER.md:553-579).  The printed listing elides the index expressions and
+ * garbles the tree condition (`if( ty ` ...); reading R18 takes them from the
+ * Rodinia kernel the figure reproduces: index = (hid+1)*HEIGHT*by + (hid+1)*ty
+ * + tx + 1 + (hid+1), index_in = HEIGHT*by + ty + 1, condition ty % 2^i == 0.
+ * Executed block by block; within a block every phase between barriers runs
+ * for all threads before the next (the barrier semantics of PAPER.md:314-351). */
+#define BP_H 16
+int oracle_bpnn_layerforward(const float* input, float* hidden, float* output, int64_t in,
+                             int64_t hid) {
+  if (hid != BP_H || in < 0 || in % BP_H || (in > 0 && (!input || !hidden || !output))) return 1;
+  const int64_t blocks = in / BP_H;
+  for (int64_t by = 0; by < blocks; ++by) {
+    float node[BP_H], w[BP_H][BP_H];
+    for (int ty = 0; ty < BP_H; ++ty) node[ty] = input[BP_H * by + ty + 1]; /* tx == 0 */
+    for (int ty = 0; ty < BP_H; ++ty)
+      for (int tx = 0; tx < BP_H; ++tx)
+        w[ty][tx] = hidden[(hid + 1) * BP_H * by + (hid + 1) * ty + tx + 1 + (hid + 1)];
+    for (int ty = 0; ty < BP_H; ++ty)
+      for (int tx = 0; tx < BP_H; ++tx) w[ty][tx] = w[ty][tx] * node[ty];
+    for (int i = 1; i <= 4; ++i) { /* log2(HEIGHT) steps */
+      const int p = 1 << i;
+      for (int ty = 0; ty < BP_H; ++ty)
+        if (ty % p == 0)
+          for (int tx = 0; tx < BP_H; ++tx) w[ty][tx] = w[ty][tx] + w[ty + p / 2][tx];
+    }
+    for (int ty = 0; ty < BP_H; ++ty)
+      for (int tx = 0; tx < BP_H; ++tx)
+        hidden[(hid + 1) * BP_H * by + (hid + 1) * ty + tx + 1 + (hid + 1)] = w[ty][tx];
+    for (int ty = 0; ty < BP_H; ++ty) output[by * hid + ty] = w[0][ty]; /* tx == 0: weights[tx][ty] */
+  }
+  return 0;
+}

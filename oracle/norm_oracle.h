@@ -91,6 +91,18 @@ int oracle_nll_backward(double* grad, const double* grad_out, const int64_t* tar
                         const float* weight, double total_weight, int64_t N, int64_t C, int64_t ld,
                         int reduction, int64_t ignore_index);
 
+/* ---- Rodinia backprop bpnn_layerforward (Fig. backprop,
+ * PAPER.md:549-584), HEIGHT = WIDTH = hid = 16, in a multiple of 16 (reading R18).
+ * Step by step in binary32 with the printed statement order and the printed
+ * shared-memory tree (no contraction):
+ *   node[ty] = input[16 by + ty + 1]
+ *   w[ty][tx] = hidden[17 (16 by + ty + 1) + tx + 1] * node[ty]
+ *   for i = 1..4: if (ty % 2^i == 0) w[ty][tx] += w[ty + 2^(i-1)][tx]
+ *   hidden[...] = w[ty][tx];   output[16 by + ty] = w[0][ty]
+ * input: fp32[in + 1]; hidden: fp32[(in + 1) * 17] (in/out); output: fp32[in]. */
+int oracle_bpnn_layerforward(const float* input, float* hidden, float* output, int64_t in,
+                             int64_t hid);
+
 #ifdef __cplusplus
 }
 #endif

@@ -508,3 +508,39 @@ def test_bulk_ring_stage_reuse_stress():
     torch.cuda.synchronize()
     expect = ((torch.arange(R, device="cuda") % 89 + 1) * C).double()
     assert torch.equal(sr, expect)
+
+
+@pytest.mark.slow
+def test_beyond_2_32_uniform_closed_form():
+    """n > 2^32 (64-bit indexing everywhere): uniform input, so S = n exactly and
+    every covered output is RN32(1 / RN32(n)) (north_star: uniform input -> 1/n)."""
+    n = 2**32 + 77
+    x = torch.ones(n, dtype=torch.float32, device="cuda")
+    out = torch.empty(n, dtype=torch.int32, device="cuda").fill_(SENTINEL_BITS).view(torch.float32)
+    S = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s = torch.zeros(1, device="cuda")
+    for mode in ("literal", "dense"):
+        L.normalize(out, x, index=mode, sum_out=s, sum_out_f64=S)
+        torch.cuda.synchronize()
+        assert S.item() == float(n)
+        sv = np.float32(s.item())
+        assert sv == np.float32(float(n))
+        q = np.float32(1.0) / sv
+        count, prefix = oracle.coverage_closed(n, mode)
+        assert prefix == (n if mode == "dense" else (n + 31) // 32 + 992)
+        ends = torch.cat([out[:4096], out[prefix - 4096:prefix]]).cpu().numpy()
+        assert np.all(ends == q)
+        if prefix < n:
+            assert torch.all(out.view(torch.int32)[prefix:prefix + 4096] == SENTINEL_BITS)
+            assert torch.all(out.view(torch.int32)[n - 4096:] == SENTINEL_BITS)
+        assert int((out[:prefix] == float(q)).sum().item()) == prefix
+
+
+def test_host_entry_pageable():
+    n = 3 * 2**20 + 11
+    x = gen.make_host(n, seed=21, dist=0)
+    out = sentinel(n)
+    s = torch.zeros(1, device="cuda")
+    L.normalize_host(out, x, index="literal", sum_out=s)
+    torch.cuda.synchronize()
+    check(x, out, np.float32(s.item()), "literal", 0)
