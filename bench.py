@@ -608,6 +608,53 @@ def run_softmax(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_backprop(args, world, rank, local):
+    """Rodinia bpnn_layerforward (Fig. backprop) as printed vs
+    with the paper's barrier elimination + mem2reg vs the register (0-barrier) form."""
+    import torch
+    import gen
+    import paper_2207_00257_b200 as L
+    n_in = 2**22
+    x = torch.empty(n_in + 1, device="cuda")
+    gen.fill_cuda(x, seed=1, dist="unit")
+    w0 = torch.empty((n_in + 1) * 17, device="cuda")
+    gen.fill_cuda(w0, seed=2, dist="unit")
+    w0 = w0.view(n_in + 1, 17)
+    h = w0.clone()
+    o = torch.empty(n_in, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    nbytes = (16 * n_in * 4) * 2 + n_in * 4 * 2  # hidden read + write, input read, output write
+    res = {}
+    for v in ("printed", "eliminated", "register"):
+        for _ in range(args.warmup):
+            L.bpnn_layerforward(x, h, o, variant=v)
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            L.bpnn_layerforward(x, h, o, variant=v)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = sum(times) / len(times)
+        res[v] = {"ms_per_step": ms, "value": nbytes / (ms / 1e3) / 1e9}
+    peak, _ = load_peak()
+    line = {"metric": "bpnn_layerforward GB/s (Rodinia backprop, Fig. backprop), in=2^22, hid=16",
+            "value": res["register"]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["register"]["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": "norm_bpnn_layerforward in=2^22 hid=16",
+                                            "l2": "flushed (256 MiB write) before every step"},
+            "variants": res, "frac_of_hbm_peak": res["register"]["value"] / peak,
+            "speedup_eliminated_over_printed": res["printed"]["ms_per_step"] / res["eliminated"]["ms_per_step"],
+            "speedup_register_over_printed": res["printed"]["ms_per_step"] / res["register"]["ms_per_step"],
+            "gpu_launches": args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_licm(args, world, rank, local):
     """Fig. 1 before/after parallel LICM on the GPU — the
     printed per-thread O(N^2) kernel, the per-block O(N^2/B) variant and the
@@ -656,7 +703,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="libnorm", choices=["libnorm", "reference"])
-    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax"])
+    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax", "backprop"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
     ap.add_argument("--numel", dest="n", type=int, default=2**32)
@@ -681,6 +728,8 @@ def main():
             run_rows(args, world, rank, local)
         elif args.workload == "softmax":
             run_softmax(args, world, rank, local)
+        elif args.workload == "backprop":
+            run_backprop(args, world, rank, local)
         elif args.workload == "licm":
             run_licm(args, world, rank, local)
         else:

@@ -185,6 +185,25 @@ norm_status_t norm_nll_backward(float* grad, const float* grad_out, const int64_
                                 int64_t C, int64_t ld, int32_t reduction, int64_t ignore_index,
                                 const norm_opts_t* o);
 
+/* ------------------------------- backprop layerforward (NEXT-4) */
+typedef enum {
+  NORM_BP_PRINTED = 0,     /* Fig. backprop as printed: shared memory, 8 barriers             */
+  NORM_BP_ELIMINATED = 1,  /* §4.1/§4.2 by hand: barriers #1, #2 removed, store/load forwarded */
+  NORM_BP_REGISTER = 2     /* one thread per (block, column), tree in registers, 0 barriers    */
+} norm_bp_variant_t;
+
+/* Rodinia backprop bpnn_layerforward (the kernel of Fig. backprop):
+ * for every 16-row block `by` of the input layer and column c < 16:
+ *   w[ty][c] = hidden[(16 by + ty + 1)(hid + 1) + c + 1] * input[16 by + ty + 1]
+ *   tree: for i = 1..4, rows ty % 2^i == 0 add row ty + 2^(i-1)   (fp32, this order)
+ *   hidden[...] <- w[ty][c];  output[16 by + c] <- w[0][c]
+ * input: device fp32[in + 1]; hidden: device fp32[(in + 1) * (hid + 1)], updated in
+ * place as the Rodinia kernel does; output: device fp32[in].  hid must be 16 and in a
+ * multiple of 16 (else NORM_ERR_UNSUPPORTED).  All variants are bitwise identical
+ * (reading R18).  o->stream is used. */
+norm_status_t norm_bpnn_layerforward(const float* input, float* hidden, float* output, int64_t in,
+                                     int64_t hid, int32_t variant, const norm_opts_t* o);
+
 /* ------------------------------------------------------------ host-only */
 
 /* Size of C(n) for the index mode; *prefix_len = L if C(n) == [0, L), else -1.

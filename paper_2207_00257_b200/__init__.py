@@ -23,6 +23,8 @@ from ._lib import (  # noqa: F401
     normalize_host,
     normalize_rows,
     softmax_rows,
+    bpnn_layerforward,
+    BP_VARIANT,
     nll_forward,
     nll_backward,
     REDUCTION,
@@ -35,7 +37,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
+    "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
     "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

@@ -51,6 +51,7 @@ def lib():
             "norm_launch_host": [vp, vp, i64, optp],
             "norm_launch_form": [vp, vp, i64, i32, optp],
             "norm_softmax_rows": [vp, vp, i64, i64, i64, i64, i32, optp],
+            "norm_bpnn_layerforward": [vp, vp, vp, i64, i64, i32, optp],
             "norm_nll_forward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
             "norm_nll_backward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
             "norm_rows": [vp, vp, i64, i64, i64, i64, optp],
@@ -214,6 +215,26 @@ def nll_backward(grad_out, logp_shape, target, total_weight, weight=None, reduct
                                    _ptr(weight), _ptr(total_weight), N, C, grad.stride(0),
                                    _enum(REDUCTION, reduction), ignore_index, ctypes.byref(o)))
     return grad
+
+
+BP_VARIANT = {"printed": 0, "eliminated": 1, "register": 2}
+
+
+def bpnn_layerforward(input_units, hidden, output, variant="register", stream=None):
+    """Rodinia backprop layer-forward (Fig. backprop): updates `hidden` in place and
+    writes the per-block column sums to `output` (norm_bpnn_layerforward)."""
+    for t, nm in ((input_units, "input"), (hidden, "hidden"), (output, "output")):
+        _check_f32(t, nm)
+        if not t.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous")
+    n_in = input_units.numel() - 1
+    hid = hidden.shape[-1] - 1 if hidden.dim() == 2 else 16
+    if hidden.numel() != (n_in + 1) * (hid + 1) or output.numel() < n_in:
+        raise ValueError("shapes: input [in+1], hidden [in+1, hid+1], output [in]")
+    o = _opts("literal", "auto", stream, None, None, device=hidden.device)
+    _check(lib().norm_bpnn_layerforward(input_units.data_ptr(), hidden.data_ptr(), output.data_ptr(),
+                                        n_in, hid, _enum(BP_VARIANT, variant), ctypes.byref(o)))
+    return hidden, output
 
 
 def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):

@@ -562,6 +562,26 @@ NORM_API norm_status_t norm_nll_backward(float* grad, const float* grad_out, con
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "nll_backward launch");
 }
 
+NORM_API norm_status_t norm_bpnn_layerforward(const float* input, float* hidden, float* output,
+                                              int64_t in, int64_t hid, int32_t variant,
+                                              const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  if (variant < NORM_BP_PRINTED || variant > NORM_BP_REGISTER)
+    return fail(NORM_ERR_INVALID_VALUE, "bad variant");
+  if (in < 0) return fail(NORM_ERR_INVALID_VALUE, "in < 0");
+  if (hid != 16 || in % 16 != 0)
+    return fail(NORM_ERR_UNSUPPORTED, "bpnn_layerforward needs hid == 16 and in % 16 == 0");
+  if (in == 0) return NORM_OK;
+  if (!input || !hidden || !output) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
+  if (in / 16 > 2147483647LL) return fail(NORM_ERR_UNSUPPORTED, "too many blocks");
+  norm_status_t s;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  cudaError_t e = launch_bpnn(input, hidden, output, in, hid, variant,
+                              static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "bpnn kernel launch");
+}
+
 NORM_API norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* prefix_len) {
   if (n < 0 || !count || !prefix_len) return fail(NORM_ERR_INVALID_VALUE, "bad argument");
   if (index != NORM_INDEX_LITERAL && index != NORM_INDEX_DENSE)

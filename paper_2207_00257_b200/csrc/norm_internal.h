@@ -103,6 +103,10 @@ cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_
                                 int64_t C, int64_t ld, int reduction, int64_t ignore_index,
                                 const DeviceInfo& d, cudaStream_t st);
 
+// NEXT-4 backprop layerforward (backprop.cu)
+cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_t in, int64_t hid,
+                        int variant, cudaStream_t st);
+
 // thread-local error detail
 void set_error(const std::string& s);
 norm_status_t fail(norm_status_t st, const std::string& s);
