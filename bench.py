@@ -255,7 +255,31 @@ def run_vector(args, world, rank, local):
         off += ln
     out = torch.empty_like(inp)
     torch.cuda.synchronize()
-    comm = L.Comm() if world > 1 and args.exchange == "nccl" else None
+    comm = None
+    exchange_note = None
+    if world > 1 and args.exchange == "p2p":
+        # the fused peer-memory exchange, cross-checked once against the gathered
+        # partials (same kernels, exchange over the process group); any failure or
+        # mismatch falls back to NCCL and is recorded in the JSON line
+        try:
+            comm = L.PeerComm()
+            s_p = torch.zeros(1, device="cuda")
+            s_g = torch.zeros(1, device="cuda")
+            comm.normalize_sharded(out, inp, mine, n, index=index, sum_out=s_p)
+            L.normalize_sharded_via(out, inp, mine, n, host_all_gather(world), index=index, sum_out=s_g)
+            torch.cuda.synchronize()
+            ok = torch.tensor([1.0 if torch.equal(s_p, s_g) else 0.0], device=_dev() if _dev() == "cuda" else "cpu")
+            import torch.distributed as dist
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() != 1.0:
+                raise RuntimeError("p2p divisor != gathered divisor")
+        except Exception as e:  # noqa: BLE001
+            exchange_note = f"p2p unavailable ({e}); fell back to nccl"
+            print(f"[bench] {exchange_note}", file=sys.stderr)
+            comm = None
+            args.exchange = "nccl"
+    if world > 1 and args.exchange == "nccl" and comm is None:
+        comm = L.Comm()
     ag = host_all_gather(world) if world > 1 and args.exchange == "host" else None
     stream = torch.cuda.current_stream()
 
@@ -341,10 +365,13 @@ def run_vector(args, world, rank, local):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"normalize n=2^{n.bit_length() - 1} fp32 (Fig. 1), {index} index, "
                                f"{'two-pass' if world > 1 or args.path == 'auto' else args.path}"
-                               + ((", coverage-balanced shards + 8 B " + ("ncclAllGather" if comm else
-                                   "all-gather over the torch.distributed group")) if world > 1 else ""),
+                               + ((", coverage-balanced shards + 8 B " + {
+                                   "nccl": "ncclAllGather", "p2p": "peer-memory stores from the reduce kernel",
+                                   "host": "all-gather over the torch.distributed group"}[args.exchange])
+                                  if world > 1 else ""),
                    "n": n, "index": index, "covered": cov_count, "algorithmic_bytes": algo,
-                   "parallelism": f"shard{world}", "exchange": args.exchange if world > 1 else None, "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
+                   "parallelism": f"shard{world}", "exchange": args.exchange if world > 1 else None,
+                   "exchange_note": exchange_note, "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
                    "l2": f"no flush: {4 * nloc / 2**30:.1f} GiB input per GPU >> 126 MB L2"},
         "frac_of_hbm_peak": value / (world * peak),
         "frac_of_datasheet": value / (world * DATASHEET_GBS),
@@ -393,7 +420,7 @@ def run_e2e(args, world, rank, local, mine, n, index):
     stream = torch.cuda.current_stream()
     comm = None
     if world > 1:
-        comm = L.Comm() if args.exchange == "nccl" else None
+        comm = {"nccl": L.Comm, "p2p": L.PeerComm}.get(args.exchange, lambda: None)()
         ag = host_all_gather(world)
         din = torch.empty(nloc, dtype=torch.float32, device="cuda")
         dout = torch.empty_like(din)
@@ -711,9 +738,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--also-dense", action="store_true", default=True)
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
-                    help="N > 1: norm_launch_sharded (ncclAllGather) or the two-phase API over "
-                         "the torch.distributed process group")
+    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p", "host"],
+                    help="N > 1: norm_launch_sharded (ncclAllGather), the fused peer-memory "
+                         "exchange (norm_launch_sharded_peer), or the two-phase API over the "
+                         "torch.distributed process group")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 untimed warm-up steps

@@ -270,6 +270,26 @@ norm_status_t norm_shard_finish(float* out_local, const float* in_local, const n
                                 int64_t n_global, const double* partials, int32_t world,
                                 const norm_opts_t* o);
 
+/* Fused exchange over peer memory (no collective launch on the data path): the
+ * reduce kernel's last CTA stores the rank's 8-byte partial straight into every
+ * rank's mailbox (CUDA IPC mappings of device memory; NVLink/NVSwitch stores on a
+ * multi-GPU box) and releases an epoch flag; the scale kernel's prologue waits
+ * for all W flags of the epoch (acquire, system scope; ~30 s timeout gives s =
+ * NaN instead of a hang) and combines the partials in rank order -- the same
+ * bits as norm_launch_sharded.  Set-up (one process per GPU, collective):
+ *   norm_peer_create -> 64-byte IPC handle of this rank's mailbox
+ *   <caller all-gathers the W handles in rank order>
+ *   norm_peer_connect(handles[W*64]) -> maps the peers' mailboxes
+ * Calls on one norm_peer_t must be issued in the same order on every rank. */
+typedef struct norm_peer norm_peer_t;
+norm_status_t norm_peer_create(norm_peer_t** peer, int32_t world, int32_t rank,
+                               unsigned char handle[64]);
+norm_status_t norm_peer_connect(norm_peer_t* peer, const unsigned char* handles);
+norm_status_t norm_peer_destroy(norm_peer_t* peer);
+norm_status_t norm_launch_sharded_peer(norm_peer_t* peer, float* out_local, const float* in_local,
+                                       const norm_shard_t* mine, int64_t n_global,
+                                       const norm_opts_t* o);
+
 /* -------------------------------------------------------------- errors */
 const char* norm_status_string(norm_status_t s);
 const char* norm_last_error(void);

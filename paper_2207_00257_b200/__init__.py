@@ -12,6 +12,7 @@ if ``libnorm.so`` is missing or the device is not sm_100, calls raise.
 """
 from ._lib import (  # noqa: F401
     Comm,
+    PeerComm,
     NormError,
     algorithmic_bytes,
     coverage,
@@ -38,6 +39,6 @@ from ._lib import (  # noqa: F401
 
 __all__ = [
     "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
-    "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "NormError", "lib", "status_string",
+    "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

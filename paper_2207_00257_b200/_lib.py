@@ -64,6 +64,10 @@ def lib():
             "norm_plan_shards": [i64, i32, i32, i32, ctypes.POINTER(NormShard)],
             "norm_launch_sharded": [vp, vp, vp, ctypes.POINTER(NormShard), i64, optp],
             "norm_shard_partial": [vp, vp, i64, optp],
+            "norm_peer_create": [ctypes.POINTER(vp), i32, i32, ctypes.c_char_p],
+            "norm_peer_connect": [vp, ctypes.c_char_p],
+            "norm_peer_destroy": [vp],
+            "norm_launch_sharded_peer": [vp, vp, vp, ctypes.POINTER(NormShard), i64, optp],
             "norm_shard_finish": [vp, vp, ctypes.POINTER(NormShard), i64, vp, i32, optp],
         }
         for name, args in sig.items():
@@ -369,4 +373,41 @@ class Comm:
     def destroy(self):
         if self._h:
             _check(lib().norm_comm_destroy(self._h))
+            self._h = None
+
+
+class PeerComm:
+    """Fused peer-memory exchange (norm_peer_*): the rank partial travels from the
+    reduce kernel straight into the peers' mailboxes; no collective is launched.
+    The 64-byte CUDA IPC handles are all-gathered through the torch.distributed
+    process group (any backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().norm_peer_create(ctypes.byref(h), self.world, self.rank, buf))
+        self._h = h
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(buf.raw), group=group)
+        allh = ctypes.create_string_buffer(b"".join(handles), 64 * self.world)
+        _check(lib().norm_peer_connect(self._h, allh))
+
+    def normalize_sharded(self, out_local, in_local, ranges, n_global, index="literal",
+                          stream=None, sum_out=None, sum_out_f64=None, events=None):
+        _check_f32(out_local, "out_local")
+        _check_f32(in_local, "in_local")
+        if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
+            raise ValueError("local buffers must hold exactly the shard's elements")
+        shard = _shard_struct(ranges)
+        o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
+        _check(lib().norm_launch_sharded_peer(self._h, out_local.data_ptr(), in_local.data_ptr(),
+                                              ctypes.byref(shard), n_global, ctypes.byref(o)))
+        return out_local
+
+    def destroy(self):
+        if self._h:
+            _check(lib().norm_peer_destroy(self._h))
             self._h = None

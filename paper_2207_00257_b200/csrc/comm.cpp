@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <string>
+#include <vector>
 
 #include "libnorm.h"
 #include "norm_internal.h"
@@ -161,7 +162,8 @@ static norm_status_t check_shard(float* out_local, const float* in_local, const 
 // prologue) and scale the locally covered elements of each owned range.
 static norm_status_t shard_finish(float* out_local, const float* in_local, const norm_shard_t* mine,
                                   int64_t n_global, const double* partials, int world,
-                                  const norm_opts_t* o, const DeviceInfo& d) {
+                                  const norm_opts_t* o, const DeviceInfo& d,
+                                  unsigned long long epoch = 0) {
   const Coverage cov = coverage_of(n_global, o->index);
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   float* so = o->sum_out;
@@ -175,7 +177,8 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
       const int64_t ce = gb + len < cov.L ? gb + len : cov.L;
       const int64_t clen = ce > gb ? ce - gb : 0;
       if (clen > 0) {
-        e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, false, st);
+        e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, false, st,
+                         epoch);
         if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
         so = nullptr;
         so64 = nullptr;
@@ -183,7 +186,7 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
       }
     } else if (cov.kind == COV_RESIDUE && len > 0) {
       e = launch_scale_residue(out_local + off, in_local + off, len, gb, cov.G, partials, world, so,
-                               so64, false, st);
+                               so64, false, st, epoch);
       if (e != cudaSuccess) return cuda_fail(e, "scale_residue launch");
       so = nullptr;
       so64 = nullptr;
@@ -191,8 +194,10 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
     }
     off += len;
   }
-  if (!launched && (so || so64)) {  // nothing covered here, but the caller wants s
-    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, false, st);
+  // Nothing covered here, but the caller wants s -- or the mailbox exchange needs
+  // every rank to wait for every epoch (see publish_partial's parity argument).
+  if (!launched && (so || so64 || epoch)) {
+    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, false, st, epoch);
     if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
   }
   return NORM_OK;
@@ -261,4 +266,111 @@ NORM_API norm_status_t norm_shard_finish(float* out_local, const float* in_local
   std::string err;
   if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
   return shard_finish(out_local, in_local, mine, n_global, partials, world, o, d);
+}
+
+// ======================================================= fused peer exchange
+// The B200-native replacement of the 8-byte ncclAllGather: the reduce kernel's
+// last CTA stores the rank partial directly into every rank's mailbox through
+// peer memory (CUDA IPC mappings; NVLink on an NVSwitch box) and the scale
+// kernel's prologue waits on the local mailbox's epoch flags.  No collective
+// launch sits between the two kernels.
+
+struct norm_peer {
+  int world = 0, rank = 0, device = -1;
+  double* mail = nullptr;        // local mailbox: [2][world] x {partial, epoch}
+  double** peer_dev = nullptr;   // device array: mailbox of rank r as mapped here
+  std::vector<void*> opened;     // IPC mappings to close
+  unsigned long long epoch = 0;
+  void* ws = nullptr;            // reduce workspace
+};
+
+NORM_API norm_status_t norm_peer_create(norm_peer_t** out, int32_t world, int32_t rank,
+                                        unsigned char handle[64]) {
+  if (!out || !handle || world < 1 || rank < 0 || rank >= world)
+    return fail(NORM_ERR_INVALID_VALUE, "bad peer arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  *out = nullptr;
+  norm_peer* p = new norm_peer();
+  p->world = world;
+  p->rank = rank;
+  cudaError_t e = cudaGetDevice(&p->device);
+  const size_t mail_bytes = ((size_t)2 * world * 2 * sizeof(double) + 4095) & ~(size_t)4095;
+  if (e == cudaSuccess) e = cudaMalloc(&p->mail, mail_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->mail, 0, mail_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->peer_dev, (size_t)world * sizeof(double*));
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws, workspace_bytes());
+  if (e == cudaSuccess) e = cudaMemset(p->ws, 0, workspace_bytes());
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p->mail);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p->mail);
+    cudaFree(p->peer_dev);
+    cudaFree(p->ws);
+    delete p;
+    return cuda_fail(e, "norm_peer_create");
+  }
+  memcpy(handle, &h, 64);
+  *out = p;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_peer_connect(norm_peer_t* p, const unsigned char* handles) {
+  if (!p || !handles) return fail(NORM_ERR_INVALID_VALUE, "bad peer arguments");
+  std::vector<double*> ptrs(p->world);
+  for (int r = 0; r < p->world; ++r) {
+    if (r == p->rank) {
+      ptrs[r] = p->mail;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + (size_t)r * 64, 64);
+    void* q = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "cudaIpcOpenMemHandle (peer mailbox)");
+    }
+    p->opened.push_back(q);
+    ptrs[r] = static_cast<double*>(q);
+  }
+  cudaError_t e = cudaMemcpy(p->peer_dev, ptrs.data(), (size_t)p->world * sizeof(double*),
+                             cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "peer table upload");
+}
+
+NORM_API norm_status_t norm_peer_destroy(norm_peer_t* p) {
+  if (!p) return NORM_OK;
+  cudaDeviceSynchronize();
+  for (void* q : p->opened) cudaIpcCloseMemHandle(q);
+  cudaFree(p->mail);
+  cudaFree(p->peer_dev);
+  cudaFree(p->ws);
+  delete p;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local,
+                                                const float* in_local, const norm_shard_t* mine,
+                                                int64_t n_global, const norm_opts_t* o) {
+  static const norm_opts_t kDef = NORM_OPTS_INIT;
+  if (!o) o = &kDef;
+  if (!p) return fail(NORM_ERR_INVALID_VALUE, "peer is NULL");
+  int64_t local = 0;
+  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  if (s != NORM_OK) return s;
+  DeviceInfo d;
+  std::string err;
+  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if (d.device != p->device) return fail(NORM_ERR_INVALID_VALUE, "current device != peer device");
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  const unsigned long long epoch = ++p->epoch;
+  Workspace ws = workspace_carve(p->ws);
+  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st,
+                                PeerPost{p->peer_dev, p->rank, p->world, epoch});
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  return shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, epoch);
 }

@@ -109,12 +109,27 @@ __device__ __forceinline__ void scale_segment(float* out, const float* in, int64
   }
 }
 
+// Fused exchange: the rank's partial goes straight from the reduce's last CTA into
+// slot [epoch & 1][rank] of every rank's mailbox (peer stores through NVLink),
+// then one system-scope fence and the epoch flags (release).  Parity double
+// buffering makes a fast rank's next epoch unable to overwrite a slot that a slow
+// rank has not read yet (the next epoch's reduce needs this epoch's scale done).
+__device__ __forceinline__ void publish_partial(const PeerPost& post, double S) {
+  if (!post.mail) return;
+  const size_t slot = ((size_t)(post.epoch & 1) * post.world + post.rank) * 2;
+  for (int r = 0; r < post.world; ++r) st_relaxed_sys_f64(post.mail[r] + slot, S);
+  __threadfence_system();
+  for (int r = 0; r < post.world; ++r)
+    st_release_sys_u64(reinterpret_cast<unsigned long long*>(post.mail[r] + slot + 1), post.epoch);
+}
+
 // --------------------------------------------------------------- reduce
 // Pass 1 of the two-pass path: S = sum in[0, n).  Persistent grid (2 CTAs/SM),
 // per-CTA partial, last-CTA ticket combines the partials in index order.
 __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
     reduce_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
-                  unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger) {
+                  unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
+                  PeerPost post) {
   // The scale kernel (PDL dependent) may be scheduled once every CTA has
   // triggered; it blocks in griddepcontrol.wait until this grid has completed.
   if (early_trigger) pdl_launch_dependents();
@@ -138,6 +153,7 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     *S_out = S;
     *ticket = 0u;  // leave the workspace reusable
+    publish_partial(post, S);
   }
 }
 
@@ -257,7 +273,8 @@ __device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char*
 // last-CTA ticket combine as reduce_kernel.
 __global__ void __launch_bounds__(BK_THREADS, 1)
     reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
-                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger) {
+                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
+                       PeerPost post) {
   if (early_trigger) pdl_launch_dependents();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
@@ -286,12 +303,35 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   if (threadIdx.x == 0) {
     *S_out = S;
     *ticket = 0u;
+    publish_partial(post, S);
   }
 }
 
-__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full) {
-  double S = __ldcg(S_parts);
-  for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
+__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full,
+                                              unsigned long long epoch = 0) {
+  double S;
+  if (epoch == 0) {
+    S = __ldcg(S_parts);
+    for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
+  } else {
+    // mailbox: wait for every rank's slot of this epoch (peer stores over NVLink)
+    const double* box = S_parts + (size_t)(epoch & 1) * nparts * 2;
+    const unsigned long long t0 = globaltimer_ns();
+    bool ok = true;
+    for (int r = 0; r < nparts && ok; ++r) {
+      const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(box + 2 * r + 1);
+      while (ld_acquire_sys_u64(flag) != epoch) {
+        if (globaltimer_ns() - t0 > 30000000000ull) { ok = false; break; }  // peer lost: no hang
+        __nanosleep(64);
+      }
+    }
+    if (!ok) {
+      S = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      S = ld_relaxed_sys_f64(box);
+      for (int r = 1; r < nparts; ++r) S += ld_relaxed_sys_f64(box + 2 * r);  // rank order
+    }
+  }
   *S_full = S;
   return (float)S;  // RN to binary32
 }
@@ -300,12 +340,12 @@ __device__ __forceinline__ float combine_parts(const double* S_parts, int nparts
 template <bool VEC, bool ALIAS>
 __global__ void __launch_bounds__(SC_THREADS)
     scale_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
-                 int nparts, float* sum_out, double* sum_out_f64) {
+                 int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
   __shared__ float s_sh;
   pdl_wait();  // S_parts are complete and visible; `in` is no longer being read
   if (threadIdx.x == 0) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S);
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
     s_sh = s;
     if (blockIdx.x == 0) {
       if (sum_out) *sum_out = s;
@@ -326,7 +366,7 @@ __global__ void __launch_bounds__(SC_THREADS)
 // tail; no store happens before the wait (out may alias in).
 __global__ void __launch_bounds__(BK_THREADS, 1)
     scale_bulk_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
-                      int nparts, float* sum_out, double* sum_out_f64) {
+                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[SB_STAGES], empty[SB_STAGES];
   __shared__ float s_sh;
@@ -339,7 +379,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   pdl_wait();
   if (ct == 0) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S);
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
     s_sh = s;
     if (blockIdx.x == 0) {
       if (sum_out) *sum_out = s;
@@ -375,12 +415,12 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
 __global__ void __launch_bounds__(256)
     scale_residue_kernel(float* out, const float* in, int64_t len, int64_t gbegin, int64_t G,
                          const double* __restrict__ S_parts, int nparts, float* sum_out,
-                         double* sum_out_f64) {
+                         double* sum_out_f64, unsigned long long epoch) {
   __shared__ float s_sh;
   pdl_wait();
   if (threadIdx.x == 0) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S);
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
     s_sh = s;
     if (blockIdx.x == 0) {
       if (sum_out) *sum_out = s;
@@ -672,7 +712,7 @@ int pdl_mode() {
 }
 
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          const DeviceInfo& d, cudaStream_t st) {
+                          const DeviceInfo& d, cudaStream_t st, PeerPost post) {
   if (n >= kBulkMinN) {
     static int configured[64] = {0};  // per device: opt in to 128 KiB of dynamic smem
     const size_t smem = BK_SMEM;
@@ -683,11 +723,11 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
       configured[d.device] = 1;
     }
     reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
-                                                        pdl_mode() == PDL_EARLY);
+                                                        pdl_mode() == PDL_EARLY, post);
     return cudaGetLastError();
   }
   reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out,
-                                                            pdl_mode() == PDL_EARLY);
+                                                            pdl_mode() == PDL_EARLY, post);
   return cudaGetLastError();
 }
 
@@ -725,7 +765,7 @@ static cudaError_t launch_maybe_pdl(Kern k, int grid, int block, bool pdl, cudaS
 
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64, const DeviceInfo& d,
-                         bool pdl, cudaStream_t st) {
+                         bool pdl, cudaStream_t st, unsigned long long epoch) {
   const int64_t per_chunk = (int64_t)SC_THREADS * SC_UNROLL * 8;
   int64_t g = (len + per_chunk - 1) / per_chunk;
   const int64_t gmax = (int64_t)d.sms * SC_CTAS_PER_SM;
@@ -742,26 +782,27 @@ cudaError_t launch_scale(float* out, const float* in, int64_t len, const double*
       configured[d.device] = 1;
     }
     return launch_maybe_pdl_smem(scale_bulk_kernel, d.sms, BK_THREADS, SB_SMEM, pdl, st, out, in,
-                                 len, S_parts, nparts, sum_out, sum_out_f64);
+                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch);
   }
   if (vec && alias)
     return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
-                            S_parts, nparts, sum_out, sum_out_f64);
+                            S_parts, nparts, sum_out, sum_out_f64, epoch);
   if (vec)
     return launch_maybe_pdl(scale_kernel<true, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
-                            S_parts, nparts, sum_out, sum_out_f64);
+                            S_parts, nparts, sum_out, sum_out_f64, epoch);
   return launch_maybe_pdl(scale_kernel<false, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
-                          S_parts, nparts, sum_out, sum_out_f64);
+                          S_parts, nparts, sum_out, sum_out_f64, epoch);
 }
 
 cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64_t gbegin,
                                  int64_t G, const double* S_parts, int nparts, float* sum_out,
-                                 double* sum_out_f64, bool pdl, cudaStream_t st) {
+                                 double* sum_out_f64, bool pdl, cudaStream_t st,
+                                 unsigned long long epoch) {
   int64_t g = (len + 255) / 256;
   if (g < 1) g = 1;
   if (g > 1024) g = 1024;
   return launch_maybe_pdl(scale_residue_kernel, (int)g, 256, pdl, st, out, in, len, gbegin, G,
-                          S_parts, nparts, sum_out, sum_out_f64);
+                          S_parts, nparts, sum_out, sum_out_f64, epoch);
 }
 
 cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,

@@ -53,22 +53,38 @@ int pdl_mode();  // NORM_PDL env knob, read once (kernels.cu)
 int reduce_grid(const DeviceInfo& d, int64_t n);
 
 // S_out <- sum of in[0, n) (fp64), via per-CTA partials and a last-block ticket.
+// Peer-memory publication of a rank's partial (fused exchange, comm.cpp).  When
+// `mail` is set, the reduce's last CTA also stores S into slot [epoch & 1][rank]
+// of every rank's mailbox (mail[r] = rank r's mailbox, mapped here) and then
+// releases the slot's epoch flag at system scope.  Mailbox layout (fp64 pairs):
+// [2 parities][world ranks] x {partial, epoch as u64}.
+struct PeerPost {
+  double* const* mail;
+  int rank, world;
+  unsigned long long epoch;
+};
+
 // n >= 2^22: TMA-bulk kernel (one CTA per SM); smaller n: LDG.E.256 kernel.
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          const DeviceInfo& d, cudaStream_t st);
+                          const DeviceInfo& d, cudaStream_t st, PeerPost post = PeerPost{nullptr, 0, 0, 0});
 
 // out[i] = in[i] / s for i in [0, len), s = (float)(S_parts[0] + ... + S_parts[nparts-1])
 // (fixed order).  Launched as a PDL dependent of the preceding kernel when pdl.
 // Block 0 writes sum_out / sum_out_f64 when non-null (also when len == 0).
+// epoch != 0: S_parts is this rank's mailbox; the prologue waits (acquire, system
+// scope, ~30 s timeout -> NaN) until all nparts slots of parity epoch & 1 carry
+// `epoch`, then combines them in rank order.
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64,
-                         const DeviceInfo& d, bool pdl, cudaStream_t st);
+                         const DeviceInfo& d, bool pdl, cudaStream_t st,
+                         unsigned long long epoch = 0);
 
 // Residue coverage (literal, G < 32): local element j is global index gbegin + j;
 // written iff (gbegin + j) % 32 < G.
 cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64_t gbegin,
                                  int64_t G, const double* S_parts, int nparts, float* sum_out,
-                                 double* sum_out_f64, bool pdl, cudaStream_t st);
+                                 double* sum_out_f64, bool pdl, cudaStream_t st,
+                                 unsigned long long epoch = 0);
 
 // One CTA: reduce, then scale C(n).  For small n (one launch, no workspace).
 cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,

@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, n, mode, balanced, q):
+def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import gen
@@ -49,26 +49,43 @@ def _worker(rank, world, port, n, mode, balanced, q):
             dist.all_gather(lst, part.cpu())
             return torch.cat(lst).cuda()
 
-        L.normalize_sharded_via(out, inp, ranges, n, ag, index=mode, sum_out=s)
+        if exchange == "gather":
+            L.normalize_sharded_via(out, inp, ranges, n, ag, index=mode, sum_out=s)
+        else:  # fused peer-memory exchange (CUDA IPC mailboxes), several epochs
+            pc = L.PeerComm()
+            ref = torch.full((nloc,), -5.0, device="cuda")
+            sref = torch.zeros(1, device="cuda")
+            L.normalize_sharded_via(ref, inp, ranges, n, ag, index=mode, sum_out=sref)
+            for _ in range(7):
+                out.fill_(-5.0)
+                pc.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s)
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref) and torch.equal(s, sref)
+            dist.barrier()
+            pc.destroy()
         torch.cuda.synchronize()
         q.put((rank, ranges, float(s.item()), out.cpu().numpy(), inp.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,mode,balanced", [
-    (2, 2**20 + 7, "literal", True),
-    (3, 2**20 + 7, "literal", False),
-    (4, 3 * 2**20 + 5, "dense", True),
-    (2, 700, "literal", True),
+@pytest.mark.parametrize("world,n,mode,balanced,exchange", [
+    (2, 2**20 + 7, "literal", True, "gather"),
+    (3, 2**20 + 7, "literal", False, "gather"),
+    (4, 3 * 2**20 + 5, "dense", True, "gather"),
+    (2, 700, "literal", True, "gather"),
+    (2, 2**22 + 7, "literal", True, "peer"),
+    (4, 3 * 2**20 + 5, "dense", True, "peer"),
+    (3, 700, "literal", True, "peer"),  # ranks without covered elements still wait every epoch
 ])
-def test_sharded_ranks_on_one_gpu(world, n, mode, balanced):
+def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange):
     import gen
     import oracle
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, n, mode, balanced, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, mode, balanced, q, exchange))
+          for r in range(world)]
     for p in ps:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
