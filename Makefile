@@ -26,7 +26,19 @@ $(PKG)/libnorm.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
+# Fault-injected builds for tests/test_gpu_faults.py only (never loaded by the product):
+# 1 = the sum drops the last element, 2 = dense index instead of literal,
+# 3 = approximate division, 7 = covered prefix off by one.
+FAULTS := 1 2 3 7
+faults: $(foreach k,$(FAULTS),$(PKG)/faults/libnorm_fault$(k).so)
+
+$(PKG)/faults/libnorm_fault%.so: $(CSRC) $(CHDR)
+	@mkdir -p $(PKG)/faults
+	$(NVCC) $(NVFLAGS) -DNORM_FAULT=$* -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> /dev/null
+
 clean:
 	rm -f oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
+	rm -rf $(PKG)/faults
 
-.PHONY: all clean
+.PHONY: all clean faults

@@ -3,7 +3,9 @@ import ctypes
 import os
 
 _DIR = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_DIR, "libnorm.so")
+# LIBNORM_SO overrides the library path; used only by tests/test_gpu_faults.py to
+# load the fault-injected builds in a subprocess.
+_SO = os.environ.get("LIBNORM_SO") or os.path.join(_DIR, "libnorm.so")
 
 INDEX = {"literal": 0, "dense": 1}
 PATH = {"auto": 0, "two_pass": 1, "fused": 2, "small": 3}

@@ -713,6 +713,9 @@ int pdl_mode() {
 
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
                           const DeviceInfo& d, cudaStream_t st, PeerPost post) {
+#if defined(NORM_FAULT) && NORM_FAULT == 1  // fault (tests only): the sum drops the last element
+  if (n > 1) n -= 1;
+#endif
   if (n >= kBulkMinN) {
     static int configured[64] = {0};  // per device: opt in to 128 KiB of dynamic smem
     const size_t smem = BK_SMEM;

@@ -35,8 +35,18 @@ norm_status_t cuda_fail(cudaError_t e, const char* what) {
 // (PAPER.md:103, 113).  tid = b + 32t, 0 <= b < G, 0 <= t < 32:
 //   G >= 32 -> every residue mod 32 occurs among b, tids fill [0, G+991]: C = [0, min(n, G+992))
 //   G <  32 -> tid mod 32 == b:  C = {x < n : x mod 32 < G}
+// NORM_FAULT: build-time fault injection for the test suite only
+// (tests/test_gpu_faults.py builds libnorm_fault<k>.so and checks that the parity
+// tests catch each fault).  Never defined in the product build.
+#ifndef NORM_FAULT
+#define NORM_FAULT 0
+#endif
+
 Coverage coverage_of(int64_t n, int index) {
   Coverage c{};
+#if NORM_FAULT == 2  // fault: the conventional (dense) index instead of Fig. 1's literal one
+  index = NORM_INDEX_DENSE;
+#endif
   c.n = n;
   c.G = n > 0 ? (n + 31) / 32 : 0;
   if (n <= 0) {
@@ -50,7 +60,11 @@ Coverage coverage_of(int64_t n, int index) {
   }
   if (c.G >= 32) {
     c.kind = COV_PREFIX;
+#if NORM_FAULT == 7  // fault: off-by-one in the covered prefix
+    c.L = c.count = (n < c.G + 991) ? n : c.G + 991;
+#else
     c.L = c.count = (n < c.G + 992) ? n : c.G + 992;
+#endif
     return c;
   }
   if (n <= 32) {  // G == 1: only tid 0
