@@ -26,6 +26,12 @@ $(PKG)/libnorm.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
+# Plain-C consumer of the C ABI (no Python): examples/normalize_c
+examples: examples/normalize_c
+examples/normalize_c: examples/normalize_c.c include/libnorm.h $(PKG)/libnorm.so
+	$(CC) -std=c11 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -l:libnorm.so \
+	    -L/usr/local/cuda/lib64 -lcudart -lm -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
+
 # Fault-injected builds for tests/test_gpu_faults.py only (never loaded by the product):
 # 1 = the sum drops the last element, 2 = dense index instead of literal,
 # 3 = approximate division, 7 = covered prefix off by one.
@@ -41,4 +47,4 @@ clean:
 	rm -f oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
 	rm -rf $(PKG)/faults
 
-.PHONY: all clean faults
+.PHONY: all clean faults examples
