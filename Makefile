@@ -32,6 +32,10 @@ examples/normalize_c: examples/normalize_c.c include/libnorm.h $(PKG)/libnorm.so
 	$(CC) -std=c11 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -l:libnorm.so \
 	    -L/usr/local/cuda/lib64 -lcudart -lm -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
+# Exhaustive division check (tests/test_gpu_division.py)
+scripts/verify_division: scripts/verify_division.cu $(PKG)/csrc/device_common.cuh
+	$(NVCC) $(ARCH) -O3 -std=c++17 -I$(PKG)/csrc -o $@ $<
+
 # Fault-injected builds for tests/test_gpu_faults.py only (never loaded by the product):
 # 1 = the sum drops the last element, 2 = dense index instead of literal,
 # 3 = approximate division, 7 = covered prefix off by one.

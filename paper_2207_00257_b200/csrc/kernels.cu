@@ -72,7 +72,7 @@ template <int THREADS, int UNROLL, bool VEC, bool ALIAS>
 __device__ __forceinline__ void scale_segment(float* out, const float* in, int64_t len, float s,
                                               int cta, int ncta) {
   if (len <= 0) return;
-  const float rs = __frcp_rn(s);
+  const Divisor dv = make_divisor(s);
   if constexpr (VEC) {
     const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(out) & 31u);
     int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
@@ -90,22 +90,22 @@ __device__ __forceinline__ void scale_segment(float* out, const float* in, int64
         v[u] = ALIAS ? ld8(ib + off + (int64_t)u * THREADS * 8)
                      : ld8_stream(ib + off + (int64_t)u * THREADS * 8);
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], s, rs));
+      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], dv));
     }
     for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
          vi += (int64_t)ncta * THREADS) {
       f8 v = ALIAS ? ld8(ib + vi * 8) : ld8_stream(ib + vi * 8);
-      st8_stream(ob + vi * 8, div8(v, s, rs));
+      st8_stream(ob + vi * 8, div8(v, dv));
     }
     if (cta == 0) {
-      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], s, rs);
+      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], dv);
       const int64_t t = head + nv * 8 + threadIdx.x;
-      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], s, rs);
+      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], dv);
     }
   } else {
     const int64_t stride = (int64_t)ncta * THREADS;
     for (int64_t i = (int64_t)cta * THREADS + threadIdx.x; i < len; i += stride)
-      out[i] = div_rn(in[i], s, rs);
+      out[i] = div_rn(in[i], dv);
   }
 }
 
@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
-  const float s = s_sh, rs = __frcp_rn(s);
+  const float s = s_sh;
+  const Divisor dv = make_divisor(s);
   constexpr int64_t CF = SB_CHUNK / 4;
   int64_t head, nchunks;
   bulk_split<CF>(in, len, &head, &nchunks);
@@ -400,7 +401,11 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
       const int i = k * BK_CONSUMERS + ct;
       const float4 a = q[2 * i], b = q[2 * i + 1];
-      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, s, rs));
+#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
+      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#else
+      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#endif
     }
     stage_release(&r.empty[r.stage]);
     r.advance();
@@ -408,8 +413,8 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
   for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
        i += (int64_t)gridDim.x * BK_CONSUMERS)
-    out[i] = div_rn(in[i], s, rs);
-  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], s, rs);
+    out[i] = div_rn(in[i], dv);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
 }
 
 __global__ void __launch_bounds__(256)
@@ -540,7 +545,8 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
   for (int k = 0; k < MAXV; ++k)
     if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
   const double S = block_sum(acc, red);
-  const float s = (float)S, rs = __frcp_rn(s);
+  const float s = (float)S;
+  const Divisor dv = make_divisor(s);
   if (threadIdx.x == 0) {
     if (sum_out) sum_out[r] = s;
     if (sum_out_f64) sum_out_f64[r] = S;
@@ -551,11 +557,11 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
     if (idx >= nvr) continue;
     const int64_t e0 = (int64_t)idx * 8;
     if (L >= 0 && e0 + 8 <= L) {
-      st8_stream(dst + e0, div8(v[k], s, rs));
+      st8_stream(dst + e0, div8(v[k], dv));
     } else if (L < 0 || e0 < L) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], s, rs);
+        if (row_covered(e0 + j, L, G)) dst[e0 + j] = div_rn(v[k].v[j], dv);
     }
   }
 }
@@ -641,7 +647,8 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
       acc += (double)((a.x + a.y) + (a.z + a.w));
     }
     const double Srow = warp_sum(acc);
-    const float s = (float)Srow, rs = __frcp_rn(s);
+    const float s = (float)Srow;
+    const Divisor dv = make_divisor(s);
     if (lane == 0) {
       if (sum_out) sum_out[r] = s;
       if (sum_out_f64) sum_out_f64[r] = Srow;
@@ -652,16 +659,16 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
       const int full4 = (int)(L >> 2);
       for (int j = lane; j < full4; j += 32) {
         const float4 a = q[j];
-        const float4 y = make_float4(div_rn(a.x, s, rs), div_rn(a.y, s, rs), div_rn(a.z, s, rs),
-                                     div_rn(a.w, s, rs));
+        const float4 y = make_float4(div_rn_fchk(a.x, dv), div_rn_fchk(a.y, dv), div_rn_fchk(a.z, dv),
+                                     div_rn_fchk(a.w, dv));
         if (vst) __stcs(reinterpret_cast<float4*>(dst) + j, y);
         else { dst[4 * j] = y.x; dst[4 * j + 1] = y.y; dst[4 * j + 2] = y.z; dst[4 * j + 3] = y.w; }
       }
       const int64_t t = (int64_t)full4 * 4 + lane;
-      if (lane < 4 && t < L) dst[t] = div_rn(src[t], s, rs);
+      if (lane < 4 && t < L) dst[t] = div_rn_fchk(src[t], dv);
     } else {
       for (int64_t i = lane; i < cols; i += 32)
-        if ((i % 32) < G) dst[i] = div_rn(src[i], s, rs);
+        if ((i % 32) < G) dst[i] = div_rn_fchk(src[i], dv);
     }
     stage_release(&empty[st]);
   }

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NC + 32, 1) sc_bulk2(float* out, const float* 
     }
   } else {
     const int ct = threadIdx.x - 32;
-    const float rs = __frcp_rn(s);
+    const Divisor dv = make_divisor(s);
     int st = 0;
     unsigned ph = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(NC + 32, 1) sc_bulk2(float* out, const float* 
 #pragma unroll 4
       for (int i = ct; i < CB / 16; i += NC) {
         float4 a = p[i];
-        a.x = div_rn(a.x, s, rs); a.y = div_rn(a.y, s, rs); a.z = div_rn(a.z, s, rs); a.w = div_rn(a.w, s, rs);
+        a.x = div_rn(a.x, dv); a.y = div_rn(a.y, dv); a.z = div_rn(a.z, dv); a.w = div_rn(a.w, dv);
         p[i] = a;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
