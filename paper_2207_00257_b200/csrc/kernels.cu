@@ -544,7 +544,7 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
 #pragma unroll
   for (int k = 0; k < MAXV; ++k)
     if (k * ROW_THREADS + (int)threadIdx.x < nvr) acc += sum8(v[k]);
-  const double S = block_sum(acc, red);
+  const double S = block_sum_1b(acc, red);  // caller alternates `red` between rows
   const float s = (float)S;
   const Divisor dv = make_divisor(s);
   if (threadIdx.x == 0) {
@@ -572,7 +572,7 @@ template <bool ALIAS, int MAXV>
 __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
     rows_vec_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                     int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
-  __shared__ double red[ROW_THREADS / 32];
+  __shared__ double red[2][ROW_THREADS / 32];  // alternated by row: one barrier per row
   const int nvr = (int)(cols >> 3);
   const int64_t step = gridDim.x;
   f8 a[MAXV], b[MAXV];
@@ -581,12 +581,12 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
   while (r < rows) {
     int64_t rn = r + step;
     if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, b);
-    row_finish<MAXV>(out + r * ld_out, nvr, a, r, L, G, red, sum_out, sum_out_f64);
+    row_finish<MAXV>(out + r * ld_out, nvr, a, r, L, G, red[0], sum_out, sum_out_f64);
     r = rn;
     if (r >= rows) break;
     rn = r + step;
     if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, a);
-    row_finish<MAXV>(out + r * ld_out, nvr, b, r, L, G, red, sum_out, sum_out_f64);
+    row_finish<MAXV>(out + r * ld_out, nvr, b, r, L, G, red[1], sum_out, sum_out_f64);
     r = rn;
   }
 }

@@ -57,18 +57,15 @@ __device__ __forceinline__ void sm_load(const float* src, int nvr, f8* v) {
 // softmax / log-softmax of one register-resident row.
 template <bool LOG, int MAXV>
 __device__ __forceinline__ void sm_finish(float* dst, int nvr, f8* v, float* redf, double* redd) {
+  // two single-barrier block reductions per row (max, then sum), on distinct
+  // buffers, so each row costs two __syncthreads; NaN propagates through max.NaN
   float m = -INFINITY;
-  int nan = 0;
 #pragma unroll
   for (int k = 0; k < MAXV; ++k)
     if (k * SM_THREADS + (int)threadIdx.x < nvr)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        m = fmaxf(m, v[k].v[j]);
-        nan |= isnan(v[k].v[j]);
-      }
-  m = block_max(m, redf);
-  if (__syncthreads_or(nan)) m = __int_as_float(0x7fffffff);  // NaN row -> NaN everywhere
+      for (int j = 0; j < 8; ++j) m = fmax_nan(m, v[k].v[j]);
+  m = block_max_1b(m, redf);
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < MAXV; ++k)
@@ -79,7 +76,7 @@ __device__ __forceinline__ void sm_finish(float* dst, int nvr, f8* v, float* red
       acc += sum8(e);
       if (!LOG) v[k] = e;
     }
-  const double S = block_sum(acc, redd);
+  const double S = block_sum_1b(acc, redd);
   if (LOG) {
     const float lse = (float)log(S);
 #pragma unroll
