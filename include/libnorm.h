@@ -290,6 +290,15 @@ norm_status_t norm_launch_sharded_peer(norm_peer_t* peer, float* out_local, cons
                                        const norm_shard_t* mine, int64_t n_global,
                                        const norm_opts_t* o);
 
+/* --------------------------------------------------------------- caches */
+/* Frees libnorm's internal per-(device, stream) caches: the ~33 KB workspaces and
+ * the norm_launch_host staging buffers (resident covered prefix, 3 x 128 MiB ring).
+ * Synchronises every device that owns a cache entry.  Later calls re-create them.
+ * Note for CUDA-graph capture: the internal workspace of a (device, stream) is
+ * allocated on its first use, which is not capturable -- make one call on the
+ * stream before capturing, or pass o->workspace. */
+norm_status_t norm_cache_release(void);
+
 /* -------------------------------------------------------------- errors */
 const char* norm_status_string(norm_status_t s);
 const char* norm_last_error(void);

@@ -15,6 +15,7 @@ from ._lib import (  # noqa: F401
     PeerComm,
     NormError,
     algorithmic_bytes,
+    cache_release,
     coverage,
     last_error,
     lib,
@@ -39,6 +40,6 @@ from ._lib import (  # noqa: F401
 
 __all__ = [
     "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
-    "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
+    "cache_release", "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

@@ -76,12 +76,19 @@ def lib():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        L.norm_cache_release.argtypes = []
+        L.norm_cache_release.restype = ctypes.c_int
         L.norm_status_string.argtypes = [ctypes.c_int]
         L.norm_status_string.restype = ctypes.c_char_p
         L.norm_last_error.argtypes = []
         L.norm_last_error.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def cache_release():
+    """Free libnorm's internal workspaces and host-staging buffers (norm_cache_release)."""
+    _check(lib().norm_cache_release())
 
 
 def status_string(s):

@@ -142,10 +142,14 @@ Workspace workspace_carve(void* base) {
   return w;
 }
 
-// Internal cache: one zeroed workspace per (device, stream), never freed (a few KB).
+// Internal cache: one zeroed workspace per (device, stream), a few KB each, kept
+// until norm_cache_release().
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, void*> g_ws_cache;
+
 static norm_status_t internal_workspace(int dev, cudaStream_t st, Workspace* ws) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, void*> cache;
+  std::mutex& mu = g_ws_mu;
+  auto& cache = g_ws_cache;
   std::lock_guard<std::mutex> lk(mu);
   auto key = std::make_pair(dev, st);
   auto it = cache.find(key);
@@ -291,10 +295,13 @@ struct HostStage {
   void* ws = nullptr;
 };
 
+static std::mutex g_hs_mu;
+static std::map<std::pair<int, cudaStream_t>, HostStage*> g_hs_cache;
+
 static norm_status_t host_stage(int dev, cudaStream_t st, int64_t resident, int64_t nchunks,
                                 HostStage** out) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, HostStage*> cache;
+  std::mutex& mu = g_hs_mu;
+  auto& cache = g_hs_cache;
   std::lock_guard<std::mutex> lk(mu);
   HostStage*& h = cache[std::make_pair(dev, st)];
   cudaError_t e;
@@ -620,6 +627,41 @@ NORM_API norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t*
   if (!bytes) return fail(NORM_ERR_INVALID_VALUE, "bytes is NULL");
   *bytes = 4 * n + 8 * count;  // read all of in once + read and write C(n)
   return NORM_OK;
+}
+
+NORM_API norm_status_t norm_cache_release(void) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& kv : g_ws_cache) {
+      cudaSetDevice(kv.first.first);
+      cudaDeviceSynchronize();
+      cudaFree(kv.second);
+    }
+    g_ws_cache.clear();
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_hs_mu);
+    for (auto& kv : g_hs_cache) {
+      HostStage* h = kv.second;
+      cudaSetDevice(kv.first.first);
+      cudaDeviceSynchronize();
+      cudaFree(h->resident);
+      for (auto& r : h->ring) cudaFree(r);
+      cudaFree(h->chunkS);
+      cudaFree(h->ws);
+      for (auto& ev : h->landed) cudaEventDestroy(ev);
+      for (auto& ev : h->slot_free) cudaEventDestroy(ev);
+      cudaEventDestroy(h->start);
+      cudaStreamDestroy(h->copy);
+      delete h;
+    }
+    g_hs_cache.clear();
+  }
+  if (cur >= 0) cudaSetDevice(cur);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "norm_cache_release");
 }
 
 NORM_API const char* norm_status_string(norm_status_t s) {

@@ -536,6 +536,20 @@ def test_beyond_2_32_uniform_closed_form():
         assert int((out[:prefix] == float(q)).sum().item()) == prefix
 
 
+def test_cache_release_and_recreate():
+    x = to_dev(gen.make_host(2**22 + 3, seed=5, dist=0))
+    a, b = torch.empty_like(x), torch.empty_like(x)
+    L.normalize(a, x, index="dense", path="two_pass")
+    h = torch.from_numpy(gen.make_host(1000, seed=1, dist=0))
+    o = torch.zeros(1000)
+    L.normalize_host(o, h)
+    torch.cuda.synchronize()
+    L.cache_release()
+    L.normalize(b, x, index="dense", path="two_pass")  # fresh workspace, same bits
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
 def test_host_entry_pageable():
     n = 3 * 2**20 + 11
     x = gen.make_host(n, seed=21, dist=0)
