@@ -326,6 +326,23 @@ def run_vector(args, world, rank, local):
     value = algo / (ms / 1e3) / 1e9
     peak, peak_src = load_peak()
     red_bytes = 4 * nloc  # the reduce kernel's algorithmic bytes per launch: read every owned element once
+    # in-run calibration on the same buffers: a torch copy stream
+    # (read + write bytes) and a torch read-only stream (torch.sum)
+    calib = {}
+    if nloc >= (1 << 24):
+        def _t(fn, reps=5):
+            fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+        cms = _t(lambda: out.copy_(inp))
+        rms = _t(lambda: torch.sum(inp))
+        calib = {"torch_copy_gbs": 8 * nloc / (cms / 1e3) / 1e9, "torch_sum_gbs": 4 * nloc / (rms / 1e3) / 1e9,
+                 "note": "same-run torch streams on this rank's buffers (copy counts read+write bytes)"}
     achieved = red_bytes / (red_ms_avg / 1e3) / 1e9
     extra = {}
     # dense-index figure on the same buffers (caption reading R1), reported beside the headline
@@ -375,12 +392,14 @@ def run_vector(args, world, rank, local):
                    "l2": f"no flush: {4 * nloc / 2**30:.1f} GiB input per GPU >> 126 MB L2"},
         "frac_of_hbm_peak": value / (world * peak),
         "frac_of_datasheet": value / (world * DATASHEET_GBS),
+        "calibration": calib,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
                      "kernel": "reduce_kernel (hoisted sum: 94% of literal bytes)",
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_instr, "instrumented_ms_per_step": ms_instr,
+                     "frac_of_same_run_read_stream": (achieved / calib["torch_sum_gbs"]) if calib else None,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

@@ -212,6 +212,15 @@ static norm_status_t check_device_ptr(const void* p, const char* name) {
   return NORM_OK;
 }
 
+// sum_out / sum_out_f64 are written by the kernels: a host pointer there would be a
+// device fault (sticky), so it is rejected up front.
+static norm_status_t check_out_ptrs(const norm_opts_t* o) {
+  norm_status_t s;
+  if (o->sum_out && (s = check_device_ptr(o->sum_out, "sum_out")) != NORM_OK) return s;
+  if (o->sum_out_f64 && (s = check_device_ptr(o->sum_out_f64, "sum_out_f64")) != NORM_OK) return s;
+  return NORM_OK;
+}
+
 static norm_status_t check_vector_args(float* out, const float* in, int64_t n) {
   if (n < 0) return fail(NORM_ERR_INVALID_VALUE, "n < 0");
   if (n == 0) return NORM_OK;
@@ -448,6 +457,7 @@ NORM_API norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, co
   if ((s = check_device(&d)) != NORM_OK) return s;
   if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
   if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
   return launch_vector(out, in, cov, o, d);
 }
 
@@ -471,6 +481,7 @@ NORM_API norm_status_t norm_launch_form(float* out, const float* in, int64_t n, 
   if ((s = check_device(&d)) != NORM_OK) return s;
   if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
   if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
   cudaError_t e = launch_unhoisted(out, in, n, o->index, form, o->sum_out, o->sum_out_f64,
                                    static_cast<cudaStream_t>(o->stream));
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "unhoisted kernel launch");
@@ -487,6 +498,7 @@ NORM_API norm_status_t norm_launch_host(float* out_host, const float* in_host, i
   if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
   return launch_host(out_host, in_host, cov, o, d);
 }
 
@@ -510,6 +522,7 @@ NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int6
   if ((s = check_device(&d)) != NORM_OK) return s;
   if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
   if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
   cudaError_t e = launch_rows(out, in, rows, cols, ld_out, ld_in, rc, o->sum_out, o->sum_out_f64, d,
                               static_cast<cudaStream_t>(o->stream));
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows_kernel launch");

@@ -299,6 +299,10 @@ def test_host_pointer_rejected():
     import ctypes
     st = L.lib().norm_launch(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(x.data_ptr()), 100)
     assert st == L._lib.STATUS.index("NORM_ERR_INVALID_VALUE")
+    d = torch.ones(100, device="cuda")
+    with pytest.raises(L.NormError):  # a host sum_out would be a device fault: rejected
+        L.normalize(d, d, sum_out=torch.zeros(1))
+    torch.cuda.synchronize()
 
 
 @pytest.mark.slow
