@@ -326,3 +326,20 @@ def test_rows_oracle():
     assert np.all(out[:, 1120:] == -3.0)  # |C(4096)| = 1120
     ones = oracle.rows(np.ones((3, 64), np.float32), "dense")
     assert np.all(ones == rn32(Fraction(1, 64)))
+
+
+def test_json_cli_spec_example():
+    # SPEC.md:510 example through the JSON CLI (I/O shape of SPEC.md:565)
+    import subprocess, sys
+    from conftest import ROOT
+    doc = json.dumps({"scalars": {}, "buffers": {"in": [1, 2, 3, 4, 5, 6, 7, 8]}})
+    r = subprocess.run([sys.executable, "-m", "oracle", doc, "--form", "thread", "--index", "dense"],
+                       capture_output=True, text=True, cwd=ROOT)
+    out = json.loads(r.stdout)
+    assert r.returncode == 0 and out["scalars"]["sum"] == 36 and out["scalars"]["adds"] == 32 * 1 * 8
+    assert out["buffers"]["out"] == [float(np.float32(k / 36)) for k in range(1, 9)]
+    r = subprocess.run([sys.executable, "-m", "oracle", doc, "--index", "literal"],
+                       capture_output=True, text=True, cwd=ROOT)
+    lit = json.loads(r.stdout)["buffers"]["out"]
+    assert lit[0] == float(np.float32(1 / 36)) and all(v is None for v in lit[1:])
+    assert subprocess.run([sys.executable, "-m", "oracle", "{bad"], capture_output=True, cwd=ROOT).returncode == 1
