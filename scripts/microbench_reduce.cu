@@ -155,13 +155,22 @@ float timeit(F f) {
   return best;
 }
 
-int main() {
+__global__ void fill_hash(float* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)(i * 2654435761u) ^ (uint32_t)(i >> 7);
+    p[i] = 0.5f + (float)(h >> 8) * 5.9604645e-08f;
+  }
+}
+
+int main(int argc, char** argv) {
   const int64_t n = 1ll << 32;
+  const bool random = argc > 1;
   float* in;
   double* out;
   if (cudaMalloc(&in, n * 4) != cudaSuccess) { printf("alloc failed\n"); return 1; }
   cudaMalloc(&out, 1 << 20);
   cudaMemset(in, 0, n * 4);
+  if (random) fill_hash<<<148 * 8, 256>>>(in, n);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double bytes = (double)n * 4;
