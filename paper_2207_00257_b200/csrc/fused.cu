@@ -1,0 +1,91 @@
+// fused.cu — reduce + grid barrier + scale in one cooperative kernel when the
+// input exceeds L2 but the covered prefix fits: the prefix is
+// read last with an L2 evict_last hint and scaled out of L2.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "stream_common.cuh"
+
+namespace lnorm {
+
+// ---------------------------------------------------------------- fused
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Single pass over HBM when the covered prefix fits in L2: one cooperative CTA
+// per SM streams the uncovered tail [L, n) through the TMA-bulk ring with an L2
+// evict_first hint, then the covered prefix [0, L) with evict_last (read LAST,
+// so it is the most recent data in L2); grid barrier; every CTA combines the
+// per-CTA partials in the same fixed order (identical s everywhere); then all
+// threads scale the prefix out of L2.  Co-residency by cooperative launch.
+template <bool VEC>
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
+                 unsigned* bar, float* sum_out, double* sum_out_f64) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ double red[BK_THREADS / 32];
+  auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
+  double acc = 0.0;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      bulk_produce<true>(r, in + L, n - L, policy_evict_first());
+      bulk_produce<true>(r, in, L, policy_evict_last());
+    }
+  } else {
+    bulk_consume(r, in + L, n - L, acc, threadIdx.x - 32);
+    bulk_consume(r, in, L, acc, threadIdx.x - 32);
+  }
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  grid_barrier(bar);  // all of `in` has been read: `out` (possibly == in) may be written
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);  // identical bits in every CTA
+  const float s = (float)S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sum_out) *sum_out = s;
+    if (sum_out_f64) *sum_out_f64 = S;
+  }
+  scale_segment<BK_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
+}
+
+cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,
+                         float* sum_out, double* sum_out_f64, const DeviceInfo& d,
+                         cudaStream_t st) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
+  void* fn = vec ? (void*)fused_kernel<true> : (void*)fused_kernel<false>;
+  static int configured[64][2] = {};
+  if (d.device < 64 && !configured[d.device][vec]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BK_SMEM);
+    if (e != cudaSuccess) return e;
+    configured[d.device][vec] = 1;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BK_THREADS, BK_SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  int grid = d.sms;  // one CTA per SM
+  int64_t n = cov.n, L = cov.L;
+  double* partials = ws.partials;
+  unsigned* bar = ws.bar;
+  void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64};
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BK_THREADS), args, BK_SMEM, st);
+}
+
+}  // namespace lnorm

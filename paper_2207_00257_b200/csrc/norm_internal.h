@@ -1,5 +1,6 @@
 // norm_internal.h — host-side internals of libnorm shared by the C ABI (libnorm.cpp),
-// the NCCL layer (comm.cpp) and the kernel launchers (kernels.cu).  Not installed.
+// the NCCL / peer layer (comm.cpp) and the kernel launchers (reduce.cu, scale.cu,
+// fused.cu, rows.cu, rowops.cu, unhoisted.cu, backprop.cu).  Not installed.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,9 +47,9 @@ struct DeviceInfo {
 bool device_info(DeviceInfo* out, std::string* err);
 
 enum PdlMode { PDL_OFF = 0, PDL_EARLY = 1, PDL_LATE = 2 };
-int pdl_mode();  // NORM_PDL env knob, read once (kernels.cu)
+int pdl_mode();  // NORM_PDL env knob, read once (reduce.cu)
 
-// ---- kernel launchers (kernels.cu).  All return the launch's cudaError_t. ----
+// ---- kernel launchers.  All return the launch's cudaError_t. ----
 // Tuning constants live next to the kernels.
 int reduce_grid(const DeviceInfo& d, int64_t n);
 

@@ -1,0 +1,143 @@
+// reduce.cu — the hoisted `sum` of Fig. 1 (hoisted by parallel
+// LICM): S = sum in[0, n) as one HBM read stream.  A TMA-bulk
+// ring kernel for n >= 2^22, an LDG.E.256 kernel below; per-CTA partials combined
+// in index order by the last CTA (ticket), optionally published to peer GPUs.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "stream_common.cuh"
+
+namespace lnorm {
+
+// Fused exchange: the rank's partial goes straight from the reduce's last CTA into
+// slot [epoch & 1][rank] of every rank's mailbox (peer stores through NVLink),
+// then one system-scope fence and the epoch flags (release).  Parity double
+// buffering makes a fast rank's next epoch unable to overwrite a slot that a slow
+// rank has not read yet (the next epoch's reduce needs this epoch's scale done).
+__device__ __forceinline__ void publish_partial(const PeerPost& post, double S) {
+  if (!post.mail) return;
+  const size_t slot = ((size_t)(post.epoch & 1) * post.world + post.rank) * 2;
+  for (int r = 0; r < post.world; ++r) st_relaxed_sys_f64(post.mail[r] + slot, S);
+  __threadfence_system();
+  for (int r = 0; r < post.world; ++r)
+    st_release_sys_u64(reinterpret_cast<unsigned long long*>(post.mail[r] + slot + 1), post.epoch);
+}
+
+// --------------------------------------------------------------- reduce
+// Pass 1 of the two-pass path: S = sum in[0, n).  Persistent grid (2 CTAs/SM),
+// per-CTA partial, last-CTA ticket combines the partials in index order.
+__global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
+    reduce_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                  unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
+                  PeerPost post) {
+  // The scale kernel (PDL dependent) may be scheduled once every CTA has
+  // triggered; it blocks in griddepcontrol.wait until this grid has completed.
+  if (early_trigger) pdl_launch_dependents();
+  __shared__ double red[RED_THREADS / 32];
+  __shared__ unsigned is_last;
+  double acc = 0.0;
+  accumulate_segment<RED_THREADS, RED_UNROLL, LD_STREAM>(in, n, blockIdx.x, gridDim.x, acc, 0);
+  if (!early_trigger) pdl_launch_dependents();
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += RED_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    *S_out = S;
+    *ticket = 0u;  // leave the workspace reusable
+    publish_partial(post, S);
+  }
+}
+
+// Pass 1, TMA-bulk variant for n >= 2^22 (one CTA per SM), then the same
+// last-CTA ticket combine as reduce_kernel.
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
+                       PeerPost post) {
+  if (early_trigger) pdl_launch_dependents();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ double red[BK_THREADS / 32];
+  __shared__ unsigned is_last;
+  auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
+  double acc = 0.0;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, n, 0);
+  } else {
+    bulk_consume(r, in, n, acc, threadIdx.x - 32);
+  }
+  if (!early_trigger) pdl_launch_dependents();
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
+  const double S = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    *S_out = S;
+    *ticket = 0u;
+    publish_partial(post, S);
+  }
+}
+
+int reduce_grid(const DeviceInfo& d, int64_t n) {
+  const int64_t chunks = (n / 8 + (int64_t)RED_THREADS * RED_UNROLL - 1) / ((int64_t)RED_THREADS * RED_UNROLL);
+  int64_t g = (int64_t)d.sms * RED_CTAS_PER_SM;
+  if (chunks < g) g = chunks < 1 ? 1 : chunks;
+  if (g > kMaxGrid) g = kMaxGrid;
+  return (int)g;
+}
+
+// Programmatic dependent launch of the scale after the reduce.  NORM_PDL=off |
+// early (trigger at the reduce's start) | late (trigger after its streaming loop,
+// the default): a tuning knob read once; every mode gives identical results.
+int pdl_mode() {
+  static int mode = [] {
+    const char* e = getenv("NORM_PDL");
+    if (e && !strcmp(e, "off")) return (int)PDL_OFF;
+    if (e && !strcmp(e, "early")) return (int)PDL_EARLY;
+    return (int)PDL_LATE;
+  }();
+  return mode;
+}
+
+cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
+                          const DeviceInfo& d, cudaStream_t st, PeerPost post) {
+#if defined(NORM_FAULT) && NORM_FAULT == 1  // fault (tests only): the sum drops the last element
+  if (n > 1) n -= 1;
+#endif
+  if (n >= kBulkMinN) {
+    static int configured[64] = {0};  // per device: opt in to 128 KiB of dynamic smem
+    const size_t smem = BK_SMEM;
+    if (d.device < 64 && !configured[d.device]) {
+      cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      configured[d.device] = 1;
+    }
+    reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
+                                                        pdl_mode() == PDL_EARLY, post);
+    return cudaGetLastError();
+  }
+  reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out,
+                                                            pdl_mode() == PDL_EARLY, post);
+  return cudaGetLastError();
+}
+
+}  // namespace lnorm

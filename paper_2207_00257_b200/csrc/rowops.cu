@@ -3,7 +3,7 @@
 // LogSoftmax ("aggregation operations like Softmax") and ClassNLLCriterion
 // updateOutput / updateGradInput (the NLL loss "uses CUDA's __syncthreads()").
 //
-// Softmax reuses the rows skeleton of kernels.cu: one row per CTA held in
+// Softmax reuses the rows skeleton of rows.cu: one row per CTA held in
 // registers (256-bit loads), the next row prefetched before the current row's
 // reductions, block max -> exp -> fp64 block sum -> scale, one HBM read and one
 // write per element.  NLL forward is a gather + deterministic two-level

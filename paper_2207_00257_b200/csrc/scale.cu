@@ -1,0 +1,216 @@
+// scale.cu — the kernel body of Fig. 1 after LICM:
+// out[i] = in[i] / s for i in the covered set C(n), other outputs untouched.
+// TMA-bulk load ring (large, co-aligned), LDG.E.256 or scalar (otherwise),
+// residue coverage (literal n <= 992), and the one-CTA small path.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "stream_common.cuh"
+
+namespace lnorm {
+
+__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full,
+                                              unsigned long long epoch = 0) {
+  double S;
+  if (epoch == 0) {
+    S = __ldcg(S_parts);
+    for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
+  } else {
+    // mailbox: wait for every rank's slot of this epoch (peer stores over NVLink)
+    const double* box = S_parts + (size_t)(epoch & 1) * nparts * 2;
+    const unsigned long long t0 = globaltimer_ns();
+    bool ok = true;
+    for (int r = 0; r < nparts && ok; ++r) {
+      const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(box + 2 * r + 1);
+      while (ld_acquire_sys_u64(flag) != epoch) {
+        if (globaltimer_ns() - t0 > 30000000000ull) { ok = false; break; }  // peer lost: no hang
+        __nanosleep(64);
+      }
+    }
+    if (!ok) {
+      S = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      S = ld_relaxed_sys_f64(box);
+      for (int r = 1; r < nparts; ++r) S += ld_relaxed_sys_f64(box + 2 * r);  // rank order
+    }
+  }
+  *S_full = S;
+  return (float)S;  // RN to binary32
+}
+
+// ---------------------------------------------------------------- scale
+template <bool VEC, bool ALIAS>
+__global__ void __launch_bounds__(SC_THREADS)
+    scale_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
+                 int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
+  __shared__ float s_sh;
+  pdl_wait();  // S_parts are complete and visible; `in` is no longer being read
+  if (threadIdx.x == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  __syncthreads();
+  scale_segment<SC_THREADS, SC_UNROLL, VEC, ALIAS>(out, in, len, s_sh, blockIdx.x, gridDim.x);
+}
+
+// Scale, TMA-bulk variant for len >= 2^22 with out/in co-aligned mod 32 B: one
+// CTA per SM, 2 x 48 KiB chunks of `in` in flight per SM via cp.async.bulk
+// (the measured optimum for a read+write stream: 6.76 TB/s vs 6.12 TB/s for
+// LDG/STG and 6.57 TB/s for cudaMemcpy D2D, scripts/microbench_scale.cu);
+// consumers divide out of shared memory and store with STG.E.256 (.cs).  The
+// producer starts streaming BEFORE griddepcontrol.wait — `in` is not written by
+// the preceding reduce — so under PDL the first chunks overlap the reduce's
+// tail; no store happens before the wait (out may alias in).
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    scale_bulk_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
+                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[SB_STAGES], empty[SB_STAGES];
+  __shared__ float s_sh;
+  auto r = bulk_ring_init<SB_STAGES, SB_CHUNK>(ring, full, empty);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, len, 0);
+    return;
+  }
+  const int ct = threadIdx.x - 32;
+  pdl_wait();
+  if (ct == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
+  const float s = s_sh;
+  const Divisor dv = make_divisor(s);
+  constexpr int64_t CF = SB_CHUNK / 4;
+  int64_t head, nchunks;
+  bulk_split<CF>(in, len, &head, &nchunks);
+  float* ob = out + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * SB_CHUNK);
+    float* oc = ob + c * CF;
+#pragma unroll
+    for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
+      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#else
+      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#endif
+    }
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    out[i] = div_rn(in[i], dv);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
+}
+
+__global__ void __launch_bounds__(256)
+    scale_residue_kernel(float* out, const float* in, int64_t len, int64_t gbegin, int64_t G,
+                         const double* __restrict__ S_parts, int nparts, float* sum_out,
+                         double* sum_out_f64, unsigned long long epoch) {
+  __shared__ float s_sh;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  __syncthreads();
+  const float s = s_sh;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if ((gbegin + j) % 32 < G) out[j] = div_rn(in[j], s);  // tid = b + 32 t, b < G
+}
+
+// ---------------------------------------------------------------- small
+// One CTA does the whole call: no workspace, one launch (latency-bound sizes).
+__global__ void __launch_bounds__(SMALL_THREADS)
+    small_kernel(float* out, const float* in, int64_t n, int kind, int64_t L, int64_t G,
+                 float* sum_out, double* sum_out_f64) {
+  __shared__ double red[SMALL_THREADS / 32];
+  double acc = 0.0;
+  accumulate_segment<SMALL_THREADS, 1, LD_PLAIN>(in, n, 0, 1, acc, 0);
+  const double S = block_sum(acc, red);  // barrier: every load precedes every store
+  const float s = (float)S;
+  if (threadIdx.x == 0) {
+    if (sum_out) *sum_out = s;
+    if (sum_out_f64) *sum_out_f64 = S;
+  }
+  if (kind == COV_PREFIX) {
+    for (int64_t i = threadIdx.x; i < L; i += SMALL_THREADS) out[i] = div_rn(in[i], s);
+  } else if (kind == COV_RESIDUE) {
+    for (int64_t i = threadIdx.x; i < n; i += SMALL_THREADS)
+      if (i % 32 < G) out[i] = div_rn(in[i], s);
+  }
+}
+
+cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
+                         int nparts, float* sum_out, double* sum_out_f64, const DeviceInfo& d,
+                         bool pdl, cudaStream_t st, unsigned long long epoch) {
+  const int64_t per_chunk = (int64_t)SC_THREADS * SC_UNROLL * 8;
+  int64_t g = (len + per_chunk - 1) / per_chunk;
+  const int64_t gmax = (int64_t)d.sms * SC_CTAS_PER_SM;
+  if (g > gmax) g = gmax;
+  if (g < 1) g = 1;
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
+  const bool alias = out == in;
+  if (vec && len >= kBulkMinN) {
+    static int configured[64] = {0};
+    if (d.device < 64 && !configured[d.device]) {
+      cudaError_t e = cudaFuncSetAttribute(scale_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)SB_SMEM);
+      if (e != cudaSuccess) return e;
+      configured[d.device] = 1;
+    }
+    return launch_maybe_pdl_smem(scale_bulk_kernel, d.sms, BK_THREADS, SB_SMEM, pdl, st, out, in,
+                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch);
+  }
+  if (vec && alias)
+    return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                            S_parts, nparts, sum_out, sum_out_f64, epoch);
+  if (vec)
+    return launch_maybe_pdl(scale_kernel<true, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                            S_parts, nparts, sum_out, sum_out_f64, epoch);
+  return launch_maybe_pdl(scale_kernel<false, false>, (int)g, SC_THREADS, pdl, st, out, in, len,
+                          S_parts, nparts, sum_out, sum_out_f64, epoch);
+}
+
+cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64_t gbegin,
+                                 int64_t G, const double* S_parts, int nparts, float* sum_out,
+                                 double* sum_out_f64, bool pdl, cudaStream_t st,
+                                 unsigned long long epoch) {
+  int64_t g = (len + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 1024) g = 1024;
+  return launch_maybe_pdl(scale_residue_kernel, (int)g, 256, pdl, st, out, in, len, gbegin, G,
+                          S_parts, nparts, sum_out, sum_out_f64, epoch);
+}
+
+cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,
+                         double* sum_out_f64, cudaStream_t st) {
+  small_kernel<<<1, SMALL_THREADS, 0, st>>>(out, in, cov.n, cov.kind, cov.L, cov.G, sum_out,
+                                            sum_out_f64);
+  return cudaGetLastError();
+}
+
+}  // namespace lnorm

@@ -1,0 +1,250 @@
+// stream_common.cuh — pieces shared by libnorm's streaming kernels (reduce.cu,
+// scale.cu, fused.cu, rows.cu): tuning constants, the LDG.E.256 segment loops,
+// the TMA-bulk (cp.async.bulk + mbarrier) ring, and the PDL launch helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device_common.cuh"
+#include "norm_internal.h"
+
+namespace lnorm {
+
+// ------------------------------------------------------------------ tuning
+constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
+constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
+constexpr int SMALL_THREADS = 1024;
+constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 4;
+constexpr int FU_SCALE_UNROLL = 8;  // fused phase 2 reads from L2: 256 B in flight per thread
+
+enum LoadKind { LD_STREAM = 0, LD_HINT = 1, LD_PLAIN = 2 };
+
+template <int K>
+__device__ __forceinline__ f8 load8(const float* p, uint64_t pol) {
+  if constexpr (K == LD_STREAM) return ld8_stream(p);
+  else if constexpr (K == LD_HINT) return ld8_policy(p, pol);
+  else return ld8(p);
+}
+
+// acc += sum of p[0, len), split over CTAs [cta, ncta) of the grid.  32-byte
+// aligned body as 8-float vectors in chunks of THREADS*UNROLL vectors (UNROLL
+// independent 256-bit loads in flight per thread); the < 8-element unaligned
+// head and < 8-element tail go to CTA 0.  The partition is a pure function of
+// (len, address mod 32, ncta), hence deterministic.
+template <int THREADS, int UNROLL, int K>
+__device__ __forceinline__ void accumulate_segment(const float* __restrict__ p, int64_t len,
+                                                   int cta, int ncta, double& acc, uint64_t pol) {
+  if (len <= 0) return;
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 31u);
+  int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
+  if (head > len) head = len;
+  const float* body = p + head;
+  const int64_t nv = (len - head) >> 3;
+  constexpr int64_t CH = (int64_t)THREADS * UNROLL;
+  const int64_t nfull = nv / CH;
+  for (int64_t c = cta; c < nfull; c += ncta) {
+    const float* q = body + (c * CH + threadIdx.x) * 8;
+    f8 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = load8<K>(q + (int64_t)u * THREADS * 8, pol);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) acc += sum8(v[u]);
+  }
+  for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
+       vi += (int64_t)ncta * THREADS)
+    acc += sum8(load8<K>(body + vi * 8, pol));
+  if (cta == 0) {
+    if ((int64_t)threadIdx.x < head) acc += (double)p[threadIdx.x];
+    const int64_t t = head + nv * 8 + threadIdx.x;
+    if (threadIdx.x < 8 && t < len) acc += (double)p[t];
+  }
+}
+
+// out[i] = in[i] / s for i in [0, len), split over CTAs; vectorised when out and
+// in are co-aligned mod 32 B (VEC), scalar otherwise.
+template <int THREADS, int UNROLL, bool VEC, bool ALIAS>
+__device__ __forceinline__ void scale_segment(float* out, const float* in, int64_t len, float s,
+                                              int cta, int ncta) {
+  if (len <= 0) return;
+  const Divisor dv = make_divisor(s);
+  if constexpr (VEC) {
+    const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(out) & 31u);
+    int64_t head = (int64_t)(((32u - mis) & 31u) >> 2);
+    if (head > len) head = len;
+    const int64_t nv = (len - head) >> 3;
+    const float* ib = in + head;
+    float* ob = out + head;
+    constexpr int64_t CH = (int64_t)THREADS * UNROLL;
+    const int64_t nfull = nv / CH;
+    for (int64_t c = cta; c < nfull; c += ncta) {
+      const int64_t off = (c * CH + threadIdx.x) * 8;
+      f8 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        v[u] = ALIAS ? ld8(ib + off + (int64_t)u * THREADS * 8)
+                     : ld8_stream(ib + off + (int64_t)u * THREADS * 8);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) st8_stream(ob + off + (int64_t)u * THREADS * 8, div8(v[u], dv));
+    }
+    for (int64_t vi = nfull * CH + (int64_t)cta * THREADS + threadIdx.x; vi < nv;
+         vi += (int64_t)ncta * THREADS) {
+      f8 v = ALIAS ? ld8(ib + vi * 8) : ld8_stream(ib + vi * 8);
+      st8_stream(ob + vi * 8, div8(v, dv));
+    }
+    if (cta == 0) {
+      if ((int64_t)threadIdx.x < head) out[threadIdx.x] = div_rn(in[threadIdx.x], dv);
+      const int64_t t = head + nv * 8 + threadIdx.x;
+      if (threadIdx.x < 8 && t < len) out[t] = div_rn(in[t], dv);
+    }
+  } else {
+    const int64_t stride = (int64_t)ncta * THREADS;
+    for (int64_t i = (int64_t)cta * THREADS + threadIdx.x; i < len; i += stride)
+      out[i] = div_rn(in[i], dv);
+  }
+}
+
+// ---- TMA-bulk streaming sum (cp.async.bulk + mbarrier ring) ----------------
+// One CTA per SM; warp 0 (one elected lane) streams 32 KiB chunks of a segment's
+// 16-byte-aligned body into a 4-stage shared-memory ring (128 KiB in flight per
+// SM: the measured sweet spot of scripts/microbench_reduce.cu, 7.56 TB/s vs
+// 7.29 TB/s for the best LDG.E.256 geometry; deeper rings lose); 8 consumer
+// warps sum each landed chunk from shared memory in a fixed per-thread order and
+// release the stage.  Chunks are dealt grid-strided; the < 32 KiB remainder and
+// the < 16 B head of each segment go through plain loads.  The ring state
+// carries across segments, so a kernel can stream several segments in a row.
+constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32;
+constexpr int BK_STAGES = 4, BK_CHUNK = 32768;  // reduce: 4 x 32 KiB in flight per SM
+constexpr int SB_STAGES = 2, SB_CHUNK = 49152;  // scale: 2 x 48 KiB (loads share HBM with stores)
+constexpr size_t BK_SMEM = (size_t)BK_STAGES * BK_CHUNK;
+// The scale ring uses 96 KiB but reserves 116 KiB (> half of the SM's 228 KiB):
+// exactly one scale CTA fits per SM, so its persistent grid spreads one CTA per
+// SM even when PDL launches it while reduce CTAs are still resident (without
+// the reservation two scale CTAs can land on one SM: measured 0.5 ms slower on
+// dense 2^32).
+constexpr size_t SB_SMEM = 116 * 1024;
+static_assert((size_t)SB_STAGES * SB_CHUNK <= SB_SMEM, "ring fits the reservation");
+constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernels are as fast
+
+template <int STAGES, int CHUNK>
+struct BulkRing {
+  static constexpr int64_t CF = CHUNK / 4;  // floats per stage
+  unsigned char* buf;
+  uint64_t* full;
+  uint64_t* empty;
+  int stage;
+  unsigned phase;
+  int issued;
+  __device__ __forceinline__ void advance() {
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+// head = floats before the first 32-byte boundary of p; then whole chunks.
+template <int64_t CF>
+__device__ __forceinline__ void bulk_split(const float* p, int64_t len, int64_t* head, int64_t* nchunks) {
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(p) & 31u);
+  int64_t h = (int64_t)(((32u - mis) & 31u) >> 2);
+  if (h > len) h = len;
+  *head = h;
+  *nchunks = (len - h) / CF;
+}
+
+// Producer side (call from one lane): issue this CTA's chunks of [p, p + len).
+template <bool HINT, int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_produce(BulkRing<STAGES, CHUNK>& r, const float* p, int64_t len,
+                                             uint64_t pol) {
+  if (len <= 0) return;
+  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
+  int64_t head, nchunks;
+  bulk_split<CF>(p, len, &head, &nchunks);
+  const float* body = p + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    if (r.issued >= STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+    mbar_arrive_expect_tx(&r.full[r.stage], CHUNK);
+    void* dst = r.buf + (size_t)r.stage * CHUNK;
+    if (HINT) bulk_g2s_hint(dst, body + c * CF, CHUNK, &r.full[r.stage], pol);
+    else bulk_g2s(dst, body + c * CF, CHUNK, &r.full[r.stage]);
+    ++r.issued;
+    r.advance();
+  }
+}
+
+// Consumer side (warps 1..8, ct = consumer thread index): acc += this CTA's share.
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_consume(BulkRing<STAGES, CHUNK>& r, const float* p, int64_t len,
+                                             double& acc, int ct) {
+  if (len <= 0) return;
+  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
+  static_assert(CHUNK % (32 * BK_CONSUMERS) == 0, "whole 8-float groups per consumer");
+  int64_t head, nchunks;
+  bulk_split<CF>(p, len, &head, &nchunks);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * CHUNK);
+#pragma unroll
+    for (int k = 0; k < CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;  // 8-float group i of the chunk
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+      f8 v = {{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+      acc += sum8(v);
+    }
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head: plain loads
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    acc += (double)p[i];
+  if (blockIdx.x == 0 && ct < head) acc += (double)p[ct];
+}
+
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char* buf, uint64_t* full,
+                                                                  uint64_t* empty) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], BK_CONSUMERS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  return BulkRing<STAGES, CHUNK>{buf, full, empty, 0, 0u, 0};
+}
+
+template <typename Kern, typename... Args>
+static inline cudaError_t launch_maybe_pdl_smem(Kern k, int grid, int block, size_t smem, bool pdl,
+                                         cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_mode() != PDL_OFF) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+template <typename Kern, typename... Args>
+static inline cudaError_t launch_maybe_pdl(Kern k, int grid, int block, bool pdl, cudaStream_t st,
+                                    Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_mode() != PDL_OFF) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+}  // namespace lnorm

@@ -3,7 +3,7 @@
 // The paper's motivating before/after: as printed, every
 // thread of normalize<<<(n+31)/32, 32>>> evaluates `sum(in, n)` — O(N^2) work;
 // the commented shared-memory variant evaluates it once per
-// block — O(N^2/B); LICM hoists it out of the kernel — O(N) (kernels.cu).
+// block — O(N^2/B); LICM hoists it out of the kernel — O(N) (reduce.cu + scale.cu).
 // These kernels run the first two forms literally (the printed launch shape,
 // the printed index expression) so the hoisted path can be timed against them.
 // `sum` is a sequential fp64 loop in index order, identical in every thread, so
