@@ -105,6 +105,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class L2Flush:
+    """Between timed steps: write a 256 MiB buffer (> the 126 MB L2, the timing
+    rule), then read a second 256 MiB buffer so the dirty lines of the write are
+    written back to HBM here, outside the timed region, instead of during the
+    next timed kernel (measured: ~18 us of foreign write-back otherwise at 2^28)."""
+
+    def __init__(self):
+        import torch
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -493,7 +509,7 @@ def run_rows(args, world, rank, local):
     gen.fill_cuda(inp, seed=2207, dist="unit", offset=r0 * C)
     inp = inp.view(rl, C)
     out = torch.empty_like(inp)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         L.normalize_rows(out, inp, index=args.index)
@@ -501,7 +517,7 @@ def run_rows(args, world, rank, local):
     barrier(world)
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush.zero_()  # 256 MiB write evicts L2 between steps
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             L.normalize_rows(out, inp, index=args.index)
@@ -523,7 +539,7 @@ def run_rows(args, world, rank, local):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"norm_rows 65536x4096 fp32, {args.index} index, rows sharded",
                    "rows": R, "cols": C, "index": args.index, "algorithmic_bytes": algo,
-                   "l2": "flushed (256 MiB write) before every step"},
+                   "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
         "frac_of_hbm_peak": value / (world * peak),
         "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
                      "frac": value / world / peak, "traffic": load_traffic("rows", args.index),
@@ -543,7 +559,7 @@ def run_paths28(args, world, rank, local):
     inp = torch.empty(n, dtype=torch.float32, device="cuda")
     gen.fill_cuda(inp, seed=2207, dist="unit")
     out = torch.empty_like(inp)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     stream = torch.cuda.current_stream()
     res = {}
     peak, src = load_peak()
@@ -552,7 +568,7 @@ def run_paths28(args, world, rank, local):
             L.normalize(out, inp, index=args.index, path=path)
         times = []
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             L.normalize(out, inp, index=args.index, path=path)
@@ -568,7 +584,7 @@ def run_paths28(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": res[best]["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"normalize n=2^28 fp32, {args.index}, best path = {best}",
-                       "l2": "flushed (256 MiB write) before every step"},
+                       "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "paths": res, "peak": peak, "gpu_launches": args.steps}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -584,7 +600,7 @@ def run_softmax(args, world, rank, local):
     gen.fill_cuda(inp, seed=2207, dist="signed")
     inp = inp.view(R, C)
     out = torch.empty_like(inp)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     stream = torch.cuda.current_stream()
     res = {}
     peak, src = load_peak()
@@ -593,7 +609,7 @@ def run_softmax(args, world, rank, local):
             L.softmax_rows(out, inp, log=log)
         times = []
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             L.softmax_rows(out, inp, log=log)
@@ -606,7 +622,7 @@ def run_softmax(args, world, rank, local):
         # torch's own kernel on the same data, for context
         times = []
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             y = (torch.log_softmax if log else torch.softmax)(inp, dim=1)
@@ -629,7 +645,7 @@ def run_softmax(args, world, rank, local):
     for name in ("nll_forward", "nll_backward"):
         times = []
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             if name == "nll_forward":
@@ -647,7 +663,7 @@ def run_softmax(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": res["softmax"]["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "norm_softmax_rows 65536x4096 fp32 (D3 signed logits)",
-                       "l2": "flushed (256 MiB write) before every step"},
+                       "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "frac_of_hbm_peak": res["softmax"]["frac"], "peak": peak, "results": res,
             "gpu_launches": args.steps}
     if rank == 0:
@@ -668,7 +684,7 @@ def run_backprop(args, world, rank, local):
     w0 = w0.view(n_in + 1, 17)
     h = w0.clone()
     o = torch.empty(n_in, device="cuda")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     stream = torch.cuda.current_stream()
     nbytes = (16 * n_in * 4) * 2 + n_in * 4 * 2  # hidden read + write, input read, output write
     res = {}
@@ -677,7 +693,7 @@ def run_backprop(args, world, rank, local):
             L.bpnn_layerforward(x, h, o, variant=v)
         times = []
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             L.bpnn_layerforward(x, h, o, variant=v)
@@ -692,7 +708,7 @@ def run_backprop(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": res["register"]["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": "norm_bpnn_layerforward in=2^22 hid=16",
-                                            "l2": "flushed (256 MiB write) before every step"},
+                                            "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "variants": res, "frac_of_hbm_peak": res["register"]["value"] / peak,
             "speedup_eliminated_over_printed": res["printed"]["ms_per_step"] / res["eliminated"]["ms_per_step"],
             "speedup_register_over_printed": res["printed"]["ms_per_step"] / res["register"]["ms_per_step"],
