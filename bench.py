@@ -294,8 +294,8 @@ def run_vector(args, world, rank, local):
             print(f"[bench] {exchange_note}", file=sys.stderr)
             comm = None
             args.exchange = "nccl"
-    if world > 1 and args.exchange == "nccl" and comm is None:
-        comm = L.Comm()
+    if world > 1 and args.exchange in ("nccl", "nccl-allreduce") and comm is None:
+        comm = L.Comm(allreduce=args.exchange == "nccl-allreduce")
     ag = host_all_gather(world) if world > 1 and args.exchange == "host" else None
     stream = torch.cuda.current_stream()
 
@@ -399,7 +399,8 @@ def run_vector(args, world, rank, local):
         "config": {"workload": f"normalize n=2^{n.bit_length() - 1} fp32 (Fig. 1), {index} index, "
                                f"{'two-pass' if world > 1 or args.path == 'auto' else args.path}"
                                + ((", coverage-balanced shards + 8 B " + {
-                                   "nccl": "ncclAllGather", "p2p": "peer-memory stores from the reduce kernel",
+                                   "nccl": "ncclAllGather", "nccl-allreduce": "ncclAllReduce",
+                                   "p2p": "peer-memory stores from the reduce kernel",
                                    "host": "all-gather over the torch.distributed group"}[args.exchange])
                                   if world > 1 else ""),
                    "n": n, "index": index, "covered": cov_count, "algorithmic_bytes": algo,
@@ -455,7 +456,8 @@ def run_e2e(args, world, rank, local, mine, n, index):
     stream = torch.cuda.current_stream()
     comm = None
     if world > 1:
-        comm = {"nccl": L.Comm, "p2p": L.PeerComm}.get(args.exchange, lambda: None)()
+        comm = {"nccl": L.Comm, "p2p": L.PeerComm,
+                "nccl-allreduce": lambda: L.Comm(allreduce=True)}.get(args.exchange, lambda: None)()
         ag = host_all_gather(world)
         din = torch.empty(nloc, dtype=torch.float32, device="cuda")
         dout = torch.empty_like(din)
@@ -773,7 +775,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--also-dense", action="store_true", default=True)
-    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p", "host"],
+    ap.add_argument("--exchange", default="p2p", choices=["nccl", "nccl-allreduce", "p2p", "host"],
                     help="N > 1: norm_launch_sharded (ncclAllGather), the fused peer-memory "
                          "exchange (norm_launch_sharded_peer), or the two-phase API over the "
                          "torch.distributed process group")

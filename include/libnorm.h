@@ -239,6 +239,15 @@ norm_status_t norm_comm_init(norm_comm_t** comm, int32_t world, int32_t rank,
                              const unsigned char id[128]);
 norm_status_t norm_comm_destroy(norm_comm_t* comm);
 
+/* How norm_launch_sharded exchanges the partials:
+ *   NORM_COMM_ALLGATHER (default): ncclAllGather of the W fp64 partials, summed in
+ *     rank order by every rank -> bit-identical s on all ranks, order pinned;
+ *   NORM_COMM_ALLREDUCE: ncclAllReduce(sum) of the fp64 partial (the north_star's
+ *     "NCCL all-reduce of a scalar"); NCCL's reduction order, identical on all
+ *     ranks for a given communicator. */
+typedef enum { NORM_COMM_ALLGATHER = 0, NORM_COMM_ALLREDUCE = 1 } norm_comm_mode_t;
+norm_status_t norm_comm_set_mode(norm_comm_t* comm, int32_t mode);
+
 /* Partition [0, n) over `world` ranks (pure host function; plan[world]).
  * DENSE, or coverage_balanced == 0: one contiguous range per rank, boundaries
  * rounded to 8 elements.  LITERAL with coverage_balanced != 0 and a prefix

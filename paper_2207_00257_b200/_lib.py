@@ -63,6 +63,7 @@ def lib():
             "norm_comm_unique_id": [ctypes.c_char_p],
             "norm_comm_init": [ctypes.POINTER(vp), i32, i32, ctypes.c_char_p],
             "norm_comm_destroy": [vp],
+            "norm_comm_set_mode": [vp, i32],
             "norm_plan_shards": [i64, i32, i32, i32, ctypes.POINTER(NormShard)],
             "norm_launch_sharded": [vp, vp, vp, ctypes.POINTER(NormShard), i64, optp],
             "norm_shard_partial": [vp, vp, i64, optp],
@@ -353,7 +354,7 @@ class Comm:
     The 128-byte NCCL unique id is created on rank 0 and broadcast through the
     torch.distributed process group (any backend)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, allreduce=False):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -366,6 +367,8 @@ class Comm:
         h = ctypes.c_void_p()
         _check(lib().norm_comm_init(ctypes.byref(h), self.world, self.rank, uid))
         self._h = h
+        if allreduce:
+            _check(lib().norm_comm_set_mode(self._h, 1))
 
     def normalize_sharded(self, out_local, in_local, ranges, n_global, index="literal",
                           stream=None, sum_out=None, sum_out_f64=None, events=None):

@@ -25,6 +25,7 @@ using namespace lnorm;
 struct norm_comm {
   ncclComm_t nccl = nullptr;
   int world = 0, rank = 0, device = -1;
+  int mode = NORM_COMM_ALLGATHER;
   double* send = nullptr;  // [1] this rank's partial
   double* recv = nullptr;  // [world] all partials, rank order
   void* ws = nullptr;      // reduce workspace (zeroed)
@@ -77,6 +78,13 @@ NORM_API norm_status_t norm_comm_init(norm_comm_t** comm, int32_t world, int32_t
     return nccl_fail(r, "ncclCommInitRank");
   }
   *comm = c;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_comm_set_mode(norm_comm_t* c, int32_t mode) {
+  if (!c || (mode != NORM_COMM_ALLGATHER && mode != NORM_COMM_ALLREDUCE))
+    return fail(NORM_ERR_INVALID_VALUE, "bad comm mode");
+  c->mode = mode;
   return NORM_OK;
 }
 
@@ -224,6 +232,11 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   // 2. exchange: W x 8 bytes over NVLink
+  if (c->mode == NORM_COMM_ALLREDUCE) {  // NCCL's own summation order; one partial back
+    ncclResult_t r = ncclAllReduce(c->send, c->recv, 1, ncclFloat64, ncclSum, c->nccl, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    return shard_finish(out_local, in_local, mine, n_global, c->recv, 1, o, d);
+  }
   ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
   // 3. rank-order combine + scale

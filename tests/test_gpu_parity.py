@@ -250,8 +250,17 @@ def test_sharded_world1():
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = L.Comm()
+        comm_ar = L.Comm(allreduce=True)
         for mode in ("literal", "dense"):
             for n in (700, 2**20 + 7):
+                x = gen.make_host(n, seed=4, dist=0)
+                ranges = L.plan_shards(n, 1, mode)[0]
+                inp = to_dev(x)
+                out = to_dev(sentinel(n))
+                s = torch.zeros(1, device="cuda")
+                comm_ar.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s)
+                torch.cuda.synchronize()
+                check(x, out.cpu().numpy(), np.float32(s.item()), mode, 0)
                 x = gen.make_host(n, seed=4, dist=0)
                 ranges = L.plan_shards(n, 1, mode)[0]
                 inp = to_dev(x)
@@ -261,6 +270,7 @@ def test_sharded_world1():
                 torch.cuda.synchronize()
                 check(x, out.cpu().numpy(), np.float32(s.item()), mode, 0)
         comm.destroy()
+        comm_ar.destroy()
     finally:
         dist.destroy_process_group()
 
