@@ -11,6 +11,22 @@ if ``libnorm.so`` is missing or the device is not sm_100, calls raise.
     (PAPER.md:98-119); uncovered outputs are untouched.
 """
 from ._lib import (  # noqa: F401
+    norm_launch,
+    norm_launch_ex,
+    norm_launch_host,
+    norm_launch_form,
+    norm_rows,
+    norm_softmax_rows,
+    norm_nll_forward,
+    norm_nll_backward,
+    norm_bpnn_layerforward,
+    norm_coverage,
+    norm_algorithmic_bytes,
+    norm_workspace_bytes,
+    norm_plan_shards,
+    norm_cache_release,
+    norm_status_string,
+    norm_last_error,
     Comm,
     PeerComm,
     NormError,

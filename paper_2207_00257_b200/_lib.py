@@ -423,3 +423,45 @@ class PeerComm:
         if self._h:
             _check(lib().norm_peer_destroy(self._h))
             self._h = None
+
+
+# ---------------------------------------------------------------------------
+# The C ABI's own names (include/libnorm.h), for callers who think in the C API.
+# Each is the same ctypes marshalling as the Pythonic spelling above.
+
+def norm_launch(out, inp):
+    """norm_launch(out, in, n): Fig. 1 launch() after LICM (literal index, current stream)."""
+    return normalize(out, inp, index="literal")
+
+
+def norm_launch_ex(out, inp, index="literal", path="auto", stream=None, sum_out=None,
+                   sum_out_f64=None, workspace=None, events=None):
+    return normalize(out, inp, index, path, stream, sum_out, sum_out_f64, workspace, events)
+
+
+def norm_launch_host(out_host, in_host, index="literal", stream=None, sum_out=None, sum_out_f64=None):
+    return normalize_host(out_host, in_host, index, stream, sum_out, sum_out_f64)
+
+
+def norm_launch_form(out, inp, form, index="literal", stream=None, sum_out=None, sum_out_f64=None):
+    return normalize_form(out, inp, form, index, stream, sum_out, sum_out_f64)
+
+
+def norm_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):
+    return normalize_rows(out, inp, index, stream, sum_out, sum_out_f64)
+
+
+def norm_softmax_rows(out, inp, kind="softmax", stream=None):
+    return softmax_rows(out, inp, log=(kind in ("log_softmax", 1)), stream=stream)
+
+
+norm_nll_forward = nll_forward
+norm_nll_backward = nll_backward
+norm_bpnn_layerforward = bpnn_layerforward
+norm_coverage = coverage
+norm_algorithmic_bytes = algorithmic_bytes
+norm_workspace_bytes = workspace_bytes
+norm_plan_shards = plan_shards
+norm_cache_release = cache_release
+norm_status_string = status_string
+norm_last_error = last_error

@@ -136,3 +136,15 @@ def test_unique_id_on_host():
     a = ctypes.create_string_buffer(128)
     assert L.lib().norm_comm_unique_id(a) == 0
     assert any(a.raw)
+
+
+def test_binding_has_c_names():
+    # the binding offers every host-callable C entry under its C name (sharded / comm
+    # entries live on Comm / PeerComm / normalize_sharded_via)
+    skip = {"norm_comm_unique_id", "norm_comm_init", "norm_comm_destroy", "norm_comm_set_mode",
+            "norm_launch_sharded", "norm_shard_partial", "norm_shard_finish", "norm_peer_create",
+            "norm_peer_connect", "norm_peer_destroy", "norm_launch_sharded_peer"}
+    for name in declared_functions():
+        if name not in skip:
+            assert hasattr(L, name), name
+    assert L.norm_coverage(2**32) == (134218720, 134218720)
