@@ -1,7 +1,7 @@
 #!/bin/bash
 # Every bench workload once (1 GPU), JSON lines into $OUT/bench_<TAG>_*.json
 OUT=${OUT:-gpurun_out}
-TAG=${TAG:-r03}
+TAG=${TAG:-r04}
 mkdir -p $OUT
 python bench.py > $OUT/bench_${TAG}_vector_literal.json 2> $OUT/bench_${TAG}_vector_literal.err
 python bench.py --index dense --no-e2e --no-cpu > $OUT/bench_${TAG}_vector_dense.json 2>/dev/null
@@ -11,5 +11,6 @@ for i in dense literal; do
 done
 python bench.py --workload softmax > $OUT/bench_${TAG}_softmax.json 2>/dev/null
 python bench.py --workload licm > $OUT/bench_${TAG}_licm.json 2>/dev/null
+python bench.py --workload backprop > $OUT/bench_${TAG}_backprop.json 2>/dev/null
 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_${TAG}_reference.json 2>/dev/null
 for f in $OUT/bench_${TAG}_*.json; do echo "$f: $(head -c 300 $f)"; done
