@@ -22,6 +22,15 @@ PATHS = ["auto", "two_pass", "fused", "small"]
 DISTS = [0, 1, 2, 3, 4]
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
 def sentinel(n):
     return np.full(n, SENTINEL_BITS, dtype=np.uint32).view(np.float32)
 
@@ -245,8 +254,8 @@ def test_host_entry(mode):
 def test_sharded_world1():
     import os
     import torch.distributed as dist
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29533")
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = L.Comm()
@@ -412,8 +421,8 @@ def test_sharded_multirange_local_semantics():
     norm_launch_sharded.  With W = 1 the divisor is the sum of the local elements."""
     import os
     import torch.distributed as dist
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = "29534"
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = L.Comm()
