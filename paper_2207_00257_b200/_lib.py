@@ -392,20 +392,37 @@ class PeerComm:
     """Fused peer-memory exchange (norm_peer_*): the rank partial travels from the
     reduce kernel straight into the peers' mailboxes; no collective is launched.
     The 64-byte CUDA IPC handles are all-gathered through the torch.distributed
-    process group (any backend)."""
+    process group (any backend).  Set-up failures are agreed on collectively, so
+    either every rank gets a PeerComm or every rank raises (callers can fall
+    back consistently)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._h = None
+
+        def agree(ok, what):
+            flags = [None] * self.world
+            dist.all_gather_object(flags, (bool(ok), what), group=group)
+            bad = [f"rank {r}: {w}" for r, (o, w) in enumerate(flags) if not o]
+            if bad:
+                if self._h:
+                    lib().norm_peer_destroy(self._h)
+                    self._h = None
+                raise RuntimeError("peer exchange unavailable: " + "; ".join(bad))
+
         h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(64)
-        _check(lib().norm_peer_create(ctypes.byref(h), self.world, self.rank, buf))
-        self._h = h
+        st = lib().norm_peer_create(ctypes.byref(h), self.world, self.rank, buf)
+        if st == 0:
+            self._h = h
+        agree(st == 0, "" if st == 0 else f"norm_peer_create: {last_error()}")
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(buf.raw), group=group)
         allh = ctypes.create_string_buffer(b"".join(handles), 64 * self.world)
-        _check(lib().norm_peer_connect(self._h, allh))
+        st = lib().norm_peer_connect(self._h, allh)
+        agree(st == 0, "" if st == 0 else f"norm_peer_connect: {last_error()}")
 
     def normalize_sharded(self, out_local, in_local, ranges, n_global, index="literal",
                           stream=None, sum_out=None, sum_out_f64=None, events=None):
