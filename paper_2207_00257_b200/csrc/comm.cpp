@@ -1,13 +1,16 @@
-// comm.cpp — multi-GPU layer of libnorm: NCCL communicator, shard planner and the
-// sharded normalize (one process per GPU, NVLink 5 / NVSwitch).
+// comm.cpp — multi-GPU layer of libnorm: shard planner, NCCL communicator, the
+// fused peer-memory exchange, and the sharded normalize (one process per GPU,
+// NVLink 5 / NVSwitch).
 //
 // The method's only cross-GPU exchange is the hoisted `sum`:
-// each rank reduces its shard to an fp64 partial S_k (8 bytes), one ncclAllGather
-// gives every rank all W partials, and the scale kernel's prologue combines them
-// in rank order — an all-reduce whose order is pinned, so every rank divides by
-// bit-identical s, run after run.  An 8-byte message is pure latency, so NCCL's
-// LL protocol is the right tool; there is nothing to overlap it with because the
-// scale cannot start before s exists.
+// each rank reduces its shard to an fp64 partial S_k (8 bytes), the W partials
+// reach every rank, and the scale kernel's prologue combines them in rank order
+// — an all-reduce whose order is pinned, so every rank divides by bit-identical
+// s, run after run.  Three carriers: the reduce kernel's own
+// peer stores into every rank's mailbox (norm_launch_sharded_peer: no collective
+// launch at all), ncclAllGather / ncclAllReduce (norm_launch_sharded), or any
+// caller collective between norm_shard_partial and norm_shard_finish.  The
+// message is 8 bytes, pure latency; the scale cannot start before s exists.
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <string.h>
