@@ -111,6 +111,18 @@ norm_status_t norm_launch(float* out, const float* in, int64_t n);
 /* As norm_launch with options (NULL o = NORM_OPTS_INIT). */
 norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, const norm_opts_t* o);
 
+/* A call captured once as a CUDA graph (its 1-2 kernels and their programmatic
+ * dependency) with its own workspace; every norm_graph_launch replays it on
+ * `stream` with one cudaGraphLaunch (launch-bound sizes: ~1 host launch instead
+ * of two).  Pointers, n and opts are fixed at creation (o->stream and the event
+ * fields are ignored).  Launches of one graph must be stream-ordered with
+ * respect to each other (they share the workspace). */
+typedef struct norm_graph norm_graph_t;
+norm_status_t norm_graph_create(norm_graph_t** graph, float* out, const float* in, int64_t n,
+                                const norm_opts_t* o);
+norm_status_t norm_graph_launch(norm_graph_t* graph, void* stream);
+norm_status_t norm_graph_destroy(norm_graph_t* graph);
+
 /* End-to-end variant on HOST buffers: out_host/in_host are host fp32[n] (pinned
  * memory gives asynchronous, overlapped copies; pageable memory works but the
  * copies serialise).  libnorm streams `in` to the device in chunks, reduces each

@@ -37,6 +37,8 @@ from ._lib import (  # noqa: F401
     lib,
     normalize,
     normalize_form,
+    NormGraph,
+    norm_graph_create,
     FORM,
     normalize_host,
     normalize_rows,
@@ -55,7 +57,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
+    "normalize", "normalize_form", "NormGraph", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
     "cache_release", "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

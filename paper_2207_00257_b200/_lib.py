@@ -52,6 +52,9 @@ def lib():
             "norm_launch_ex": [vp, vp, i64, optp],
             "norm_launch_host": [vp, vp, i64, optp],
             "norm_launch_form": [vp, vp, i64, i32, optp],
+            "norm_graph_create": [ctypes.POINTER(vp), vp, vp, i64, optp],
+            "norm_graph_launch": [vp, vp],
+            "norm_graph_destroy": [vp],
             "norm_softmax_rows": [vp, vp, i64, i64, i64, i64, i32, optp],
             "norm_bpnn_layerforward": [vp, vp, vp, i64, i64, i32, optp],
             "norm_nll_forward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
@@ -249,6 +252,38 @@ def bpnn_layerforward(input_units, hidden, output, variant="register", stream=No
     _check(lib().norm_bpnn_layerforward(input_units.data_ptr(), hidden.data_ptr(), output.data_ptr(),
                                         n_in, hid, _enum(BP_VARIANT, variant), ctypes.byref(o)))
     return hidden, output
+
+
+class NormGraph:
+    """One normalize call captured as a CUDA graph (norm_graph_create): replay with
+    launch(stream) -- one cudaGraphLaunch for the reduce + scale pair."""
+
+    def __init__(self, out, inp, index="literal", path="auto", sum_out=None, sum_out_f64=None):
+        _check_f32(out, "out")
+        _check_f32(inp, "inp")
+        if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
+            raise ValueError("out and inp must be contiguous with equal numel")
+        self._keep = (out, inp, sum_out, sum_out_f64)  # the graph holds raw pointers
+        o = _opts(index, path, None, sum_out, sum_out_f64, device=inp.device)
+        h = ctypes.c_void_p()
+        _check(lib().norm_graph_create(ctypes.byref(h), out.data_ptr(), inp.data_ptr(), inp.numel(),
+                                       ctypes.byref(o)))
+        self._h = h
+        self._device = inp.device
+
+    def launch(self, stream=None):
+        _check(lib().norm_graph_launch(self._h, _stream_handle(stream, self._device)))
+
+    def destroy(self):
+        if self._h:
+            _check(lib().norm_graph_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):
@@ -472,6 +507,7 @@ def norm_softmax_rows(out, inp, kind="softmax", stream=None):
     return softmax_rows(out, inp, log=(kind in ("log_softmax", 1)), stream=stream)
 
 
+norm_graph_create = NormGraph
 norm_nll_forward = nll_forward
 norm_nll_backward = nll_backward
 norm_bpnn_layerforward = bpnn_layerforward

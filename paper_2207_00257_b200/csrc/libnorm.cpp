@@ -461,6 +461,84 @@ NORM_API norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, co
   return launch_vector(out, in, cov, o, d);
 }
 
+// ---- CUDA-graph plans: the whole call (1 or 2 kernels) as one cudaGraphLaunch ----
+struct norm_graph {
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  void* ws = nullptr;
+  int device = -1;
+};
+
+NORM_API norm_status_t norm_graph_create(norm_graph_t** out_g, float* out, const float* in,
+                                         int64_t n, const norm_opts_t* o) {
+  if (!out_g) return fail(NORM_ERR_INVALID_VALUE, "graph is NULL");
+  *out_g = nullptr;
+  if (!o) o = &kDefaultOpts;
+  norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
+  if ((s = check_vector_args(out, in, n)) != NORM_OK) return s;
+  const Coverage cov = coverage_of(n, o->index);
+  if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
+  DeviceInfo d;
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if (n > 0) {
+    if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
+    if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+    if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  }
+  norm_graph* g = new norm_graph();
+  g->device = d.device;
+  auto bail = [&](norm_status_t st) {
+    if (g->cap) cudaStreamDestroy(g->cap);
+    cudaFree(g->ws);
+    delete g;
+    return st;
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&g->ws, workspace_bytes());
+  if (e == cudaSuccess) e = cudaMemset(g->ws, 0, workspace_bytes());
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return bail(cuda_fail(e, "graph set-up"));
+  }
+  norm_opts_t oc = *o;
+  oc.stream = g->cap;
+  oc.workspace = g->ws;
+  oc.workspace_bytes = workspace_bytes();
+  oc.ev_reduce_begin = oc.ev_reduce_end = nullptr;
+  if ((e = cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaStreamBeginCapture"));
+  s = n > 0 ? launch_vector(out, in, cov, &oc, d) : NORM_OK;
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(g->cap, &graph);
+  if (s != NORM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return bail(s);
+  }
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamEndCapture"));
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGraphInstantiate"));
+  *out_g = g;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_graph_launch(norm_graph_t* g, void* stream) {
+  if (!g) return fail(NORM_ERR_INVALID_VALUE, "graph is NULL");
+  cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "cudaGraphLaunch");
+}
+
+NORM_API norm_status_t norm_graph_destroy(norm_graph_t* g) {
+  if (!g) return NORM_OK;
+  cudaDeviceSynchronize();
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->cap) cudaStreamDestroy(g->cap);
+  cudaFree(g->ws);
+  delete g;
+  return NORM_OK;
+}
+
 NORM_API norm_status_t norm_launch(float* out, const float* in, int64_t n) {
   return norm_launch_ex(out, in, n, nullptr);
 }

@@ -29,3 +29,19 @@ for n in (1024, 16384, 65536, 2**18, 2**20 + 7, 2**22, 2**24):
         torch.cuda.synchronize()
         row.append(f"{path}={a.elapsed_time(b) * 1e3 / 500:7.2f}us")
     print(f"n={n:>9}: " + "  ".join(row))
+
+# host-side cost per call: eager Python binding vs a replayed NormGraph (n = 2^20 + 7)
+import time
+n = 2**20 + 7
+x = torch.rand(n, device="cuda")
+y = torch.empty_like(x)
+g = L.NormGraph(y, x)
+for f, name in ((lambda: L.normalize(y, x), "eager normalize"), (g.launch, "NormGraph.launch")):
+    for _ in range(200):
+        f()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(2000):
+        f()
+    torch.cuda.synchronize()
+    print(f"{name}: {(time.perf_counter() - t) / 2000 * 1e6:.2f} us/call (host + device, back to back)")

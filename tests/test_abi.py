@@ -143,7 +143,8 @@ def test_binding_has_c_names():
     # entries live on Comm / PeerComm / normalize_sharded_via)
     skip = {"norm_comm_unique_id", "norm_comm_init", "norm_comm_destroy", "norm_comm_set_mode",
             "norm_launch_sharded", "norm_shard_partial", "norm_shard_finish", "norm_peer_create",
-            "norm_peer_connect", "norm_peer_destroy", "norm_launch_sharded_peer"}
+            "norm_peer_connect", "norm_peer_destroy", "norm_launch_sharded_peer",
+            "norm_graph_launch", "norm_graph_destroy"}
     for name in declared_functions():
         if name not in skip:
             assert hasattr(L, name), name

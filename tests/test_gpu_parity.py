@@ -581,3 +581,21 @@ def test_host_entry_pageable():
     L.normalize_host(out, x, index="literal", sum_out=s)
     torch.cuda.synchronize()
     check(x, out, np.float32(s.item()), "literal", 0)
+
+
+@pytest.mark.parametrize("n,mode,path", [(1000, "literal", "auto"), (2**20 + 7, "literal", "auto"),
+                                         (3 * 2**20 + 5, "dense", "two_pass"),
+                                         (2**22 + 9, "dense", "fused"), (2**23 + 1, "literal", "auto")])
+def test_graph_plan_matches_eager(n, mode, path):
+    x = to_dev(gen.make_host(n, seed=n % 101, dist=0))
+    ref = to_dev(sentinel(n))
+    out = to_dev(sentinel(n))
+    s = torch.zeros(1, device="cuda")
+    L.normalize(ref, x, index=mode, path=path)
+    g = L.NormGraph(out, x, index=mode, path=path, sum_out=s)
+    for _ in range(3):
+        g.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    check(x.cpu().numpy(), out.cpu().numpy(), np.float32(s.item()), mode, 0)
+    g.destroy()
