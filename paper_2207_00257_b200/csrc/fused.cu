@@ -63,12 +63,6 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     if (sum_out_f64) *sum_out_f64 = S;
   }
   scale_segment<BK_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
-  // the prefix's evict_last lines have served their reuse: back to evict_normal,
-  // so they cannot linger into the next call
-  const char* pb = reinterpret_cast<const char*>(in);
-  for (int64_t o = ((int64_t)blockIdx.x * BK_THREADS + threadIdx.x) * 128; o < L * 4;
-       o += (int64_t)gridDim.x * BK_THREADS * 128)
-    l2_demote_line(pb + o);
 }
 
 cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,

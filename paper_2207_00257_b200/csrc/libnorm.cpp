@@ -247,7 +247,6 @@ static norm_status_t check_literal_grid(const Coverage& c, int index) {
 //  * otherwise two-pass.
 constexpr int64_t kSmallN = 1 << 17;
 
-
 static int choose_path(const Coverage& cov, const norm_opts_t* o, const DeviceInfo& d) {
   if (o->path != NORM_PATH_AUTO) return o->path;
   if (cov.n <= kSmallN) return NORM_PATH_SMALL;
@@ -274,17 +273,12 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
     e = launch_fused(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
     return e == cudaSuccess ? NORM_OK : cuda_fail(e, "fused_kernel cooperative launch");
   }
-  // L2 retention: the reduce reads the last R covered elements last (evict_last)
-  // and the scale starts with them
-  const int64_t R = cov.kind == COV_PREFIX ? retain_elems(cov.n, cov.L, d) : 0;
-  const int64_t kb = cov.L - R;
   if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  e = launch_reduce(in, cov.n, ws, ws.S, d, st, PeerPost{nullptr, 0, 0, 0}, R ? kb : 0, R ? cov.L : 0);
+  e = launch_reduce(in, cov.n, ws, ws.S, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   if (cov.kind == COV_PREFIX)
-    e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st, 0,
-                     R ? kb : 0, R > 0);
+    e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st);
   else
     e = launch_scale_residue(out, in, cov.n, 0, cov.G, ws.S, 1, o->sum_out, o->sum_out_f64, true, st);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "scale_kernel launch");

@@ -66,17 +66,8 @@ struct PeerPost {
 };
 
 // n >= 2^22: TMA-bulk kernel (one CTA per SM); smaller n: LDG.E.256 kernel.
-// [kb, ke): L2 retention window read last with evict_last (bulk kernel only;
-// kb == ke: none) — see retain_window().
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          const DeviceInfo& d, cudaStream_t st, PeerPost post = PeerPost{nullptr, 0, 0, 0},
-                          int64_t kb = 0, int64_t ke = 0);
-
-// Elements of the covered prefix [0, len) that the two-pass path keeps in L2
-// between the reduce and the scale: the window [len - R, len), R = min(len,
-// NORM_RETAIN_BYTES / 4) (default kRetainBytes, 0 disables).  Only when the
-// input does not fit in L2 anyway (n * 4 > L2) and the bulk reduce runs.
-int64_t retain_elems(int64_t n, int64_t len, const DeviceInfo& d);
+                          const DeviceInfo& d, cudaStream_t st, PeerPost post = PeerPost{nullptr, 0, 0, 0});
 
 // out[i] = in[i] / s for i in [0, len), s = (float)(S_parts[0] + ... + S_parts[nparts-1])
 // (fixed order).  Launched as a PDL dependent of the preceding kernel when pdl.
@@ -84,13 +75,10 @@ int64_t retain_elems(int64_t n, int64_t len, const DeviceInfo& d);
 // epoch != 0: S_parts is this rank's mailbox; the prologue waits (acquire, system
 // scope, ~30 s timeout -> NaN) until all nparts slots of parity epoch & 1 carry
 // `epoch`, then combines them in rank order.
-// The bulk kernel scales [first, len) before [0, first); demote: [first, len) is
-// the L2 retention window of the preceding reduce, whose lines are demoted to
-// evict_normal once read (retention never outlives the call).
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64,
                          const DeviceInfo& d, bool pdl, cudaStream_t st,
-                         unsigned long long epoch = 0, int64_t first = 0, bool demote = false);
+                         unsigned long long epoch = 0);
 
 // Residue coverage (literal, G < 32): local element j is global index gbegin + j;
 // written iff (gbegin + j) % 32 < G.

@@ -59,16 +59,11 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
 }
 
 // Pass 1, TMA-bulk variant for n >= 2^22 (one CTA per SM), then the same
-// last-CTA ticket combine as reduce_kernel.  Retention window [kb, ke) (kb < ke):
-// the stream visits [ke, n), [0, kb) with an L2 evict_first hint and the window
-// LAST with evict_last, so the scale that follows (which starts at kb) finds
-// those bytes in L2 instead of re-reading them from HBM.  kb == ke: one plain
-// stream over [0, n).  Either way the partition is a pure function of
-// (n, kb, ke, address mod 32, grid), hence deterministic.
+// last-CTA ticket combine as reduce_kernel.
 __global__ void __launch_bounds__(BK_THREADS, 1)
     reduce_bulk_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
                        unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
-                       PeerPost post, int64_t kb, int64_t ke) {
+                       PeerPost post) {
   if (early_trigger) pdl_launch_dependents();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
@@ -77,24 +72,9 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   double acc = 0.0;
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      if (kb < ke) {
-        const uint64_t ef = policy_evict_first();
-        bulk_produce<true>(r, in + ke, n - ke, ef);
-        bulk_produce<true>(r, in, kb, ef);
-        bulk_produce<true>(r, in + kb, ke - kb, policy_evict_last());
-      } else {
-        bulk_produce<false>(r, in, n, 0);
-      }
-    }
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, n, 0);
   } else {
-    if (kb < ke) {
-      bulk_consume(r, in + ke, n - ke, acc, threadIdx.x - 32);
-      bulk_consume(r, in, kb, acc, threadIdx.x - 32);
-      bulk_consume(r, in + kb, ke - kb, acc, threadIdx.x - 32);
-    } else {
-      bulk_consume(r, in, n, acc, threadIdx.x - 32);
-    }
+    bulk_consume(r, in, n, acc, threadIdx.x - 32);
   }
   if (!early_trigger) pdl_launch_dependents();
   const double b = block_sum(acc, red);
@@ -137,25 +117,8 @@ int pdl_mode() {
   return mode;
 }
 
-// Two-pass L2 retention (norm_internal.h): bytes of the covered prefix's end
-// that the reduce reads last with evict_last and the scale reads first.
-// NORM_RETAIN_BYTES overrides (0 disables); read once.
-constexpr int64_t kRetainBytes = 48ll << 20;
-
-int64_t retain_elems(int64_t n, int64_t len, const DeviceInfo& d) {
-  static const int64_t bytes = [] {
-    const char* e = getenv("NORM_RETAIN_BYTES");
-    return e ? (int64_t)strtoll(e, nullptr, 10) : kRetainBytes;
-  }();
-  if (bytes <= 0 || n < kBulkMinN || (size_t)n * 4 <= d.l2_bytes || len <= 0) return 0;
-  int64_t r = bytes / 4;
-  if ((size_t)r * 4 > d.l2_bytes / 2) r = (int64_t)(d.l2_bytes / 8);
-  return r < len ? r : len;
-}
-
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
-                          const DeviceInfo& d, cudaStream_t st, PeerPost post, int64_t kb,
-                          int64_t ke) {
+                          const DeviceInfo& d, cudaStream_t st, PeerPost post) {
 #if defined(NORM_FAULT) && NORM_FAULT == 1  // fault (tests only): the sum drops the last element
   if (n > 1) n -= 1;
 #endif
@@ -168,9 +131,8 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
       if (e != cudaSuccess) return e;
       configured[d.device] = 1;
     }
-    if (!(0 <= kb && kb < ke && ke <= n)) kb = ke = 0;
     reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
-                                                        pdl_mode() == PDL_EARLY, post, kb, ke);
+                                                        pdl_mode() == PDL_EARLY, post);
     return cudaGetLastError();
   }
   reduce_kernel<<<reduce_grid(d, n), RED_THREADS, 0, st>>>(in, n, ws.partials, ws.ticket, S_out,

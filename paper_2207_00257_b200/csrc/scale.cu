@@ -67,58 +67,15 @@ __global__ void __launch_bounds__(SC_THREADS)
 // producer starts streaming BEFORE griddepcontrol.wait — `in` is not written by
 // the preceding reduce — so under PDL the first chunks overlap the reduce's
 // tail; no store happens before the wait (out may alias in).
-// [first, len) is scaled before [0, first); demote != 0: that window is the one
-// the reduce read last with evict_last, and each of its L2 lines is demoted to
-// evict_normal once consumed.
-template <int STAGES, int CHUNK>
-__device__ __forceinline__ void scale_bulk_consume(BulkRing<STAGES, CHUNK>& r, float* out,
-                                                   const float* in, int64_t len, const Divisor& dv,
-                                                   int ct, bool demote) {
-  if (len <= 0) return;
-  constexpr int64_t CF = CHUNK / 4;
-  int64_t head, nchunks;
-  bulk_split<CF>(in, len, &head, &nchunks);
-  float* ob = out + head;
-  const float* ib = in + head;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    mbar_wait(&r.full[r.stage], r.phase);
-    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * CHUNK);
-    float* oc = ob + c * CF;
-#pragma unroll
-    for (int k = 0; k < CHUNK / 32 / BK_CONSUMERS; ++k) {
-      const int i = k * BK_CONSUMERS + ct;
-      const float4 a = q[2 * i], b = q[2 * i + 1];
-#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
-      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
-#else
-      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
-#endif
-    }
-    stage_release(&r.empty[r.stage]);
-    r.advance();
-    if (demote)
-      for (int l = ct; l < CHUNK / 128; l += BK_CONSUMERS) l2_demote_line(ib + c * CF + (int64_t)l * 32);
-  }
-  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
-  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
-       i += (int64_t)gridDim.x * BK_CONSUMERS)
-    out[i] = div_rn(in[i], dv);
-  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
-}
-
 __global__ void __launch_bounds__(BK_THREADS, 1)
     scale_bulk_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
-                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch,
-                      int64_t first, int demote) {
+                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[SB_STAGES], empty[SB_STAGES];
   __shared__ float s_sh;
   auto r = bulk_ring_init<SB_STAGES, SB_CHUNK>(ring, full, empty);
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      bulk_produce<false>(r, in + first, len - first, 0);
-      bulk_produce<false>(r, in, first, 0);
-    }
+    if (threadIdx.x == 0) bulk_produce<false>(r, in, len, 0);
     return;
   }
   const int ct = threadIdx.x - 32;
@@ -133,9 +90,34 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
-  const Divisor dv = make_divisor(s_sh);
-  scale_bulk_consume(r, out + first, in + first, len - first, dv, ct, demote != 0);
-  scale_bulk_consume(r, out, in, first, dv, ct, false);
+  const float s = s_sh;
+  const Divisor dv = make_divisor(s);
+  constexpr int64_t CF = SB_CHUNK / 4;
+  int64_t head, nchunks;
+  bulk_split<CF>(in, len, &head, &nchunks);
+  float* ob = out + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * SB_CHUNK);
+    float* oc = ob + c * CF;
+#pragma unroll
+    for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
+      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#else
+      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#endif
+    }
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    out[i] = div_rn(in[i], dv);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
 }
 
 __global__ void __launch_bounds__(256)
@@ -184,8 +166,7 @@ __global__ void __launch_bounds__(SMALL_THREADS)
 
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64, const DeviceInfo& d,
-                         bool pdl, cudaStream_t st, unsigned long long epoch, int64_t first,
-                         bool demote) {
+                         bool pdl, cudaStream_t st, unsigned long long epoch) {
   const int64_t per_chunk = (int64_t)SC_THREADS * SC_UNROLL * 8;
   int64_t g = (len + per_chunk - 1) / per_chunk;
   const int64_t gmax = (int64_t)d.sms * SC_CTAS_PER_SM;
@@ -201,10 +182,8 @@ cudaError_t launch_scale(float* out, const float* in, int64_t len, const double*
       if (e != cudaSuccess) return e;
       configured[d.device] = 1;
     }
-    if (!(0 <= first && first < len)) first = 0, demote = false;
     return launch_maybe_pdl_smem(scale_bulk_kernel, d.sms, BK_THREADS, SB_SMEM, pdl, st, out, in,
-                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch, first,
-                                 (int)demote);
+                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch);
   }
   if (vec && alias)
     return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
