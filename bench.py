@@ -491,11 +491,27 @@ def run_e2e(args, world, rank, local, mine, n, index):
     ms = max_over_ranks(a.elapsed_time(b) / steps, world)
     if comm:
         comm.destroy()
+    # the link this number is bound by: a plain pinned H2D copy of 1 GiB pieces of
+    # the same host buffer (the e2e step moves 4n bytes host -> device)
+    piece = min(nloc, 1 << 28)
+    dbuf = torch.empty(piece, dtype=torch.float32, device="cuda")
+    dbuf.copy_(host_in[:piece], non_blocking=True)
+    k = max(1, min(4, nloc // piece))
+    a.record(stream)
+    for j in range(k):
+        dbuf.copy_(host_in[j * piece:(j + 1) * piece], non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = 4 * piece * k / (a.elapsed_time(b) / 1e3) / 1e9
+    del dbuf
     algo = L.algorithmic_bytes(n, index)
     h2d = 4 * n
     d2h = 4 * count
+    step_h2d_gbs = h2d / world / (ms / 1e3) / 1e9
     return {"value": algo / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "pcie_h2d_gbs": h2d_gbs, "step_h2d_gbs": step_h2d_gbs,
+            "frac_of_pcie_h2d": step_h2d_gbs / h2d_gbs,
             "api": "norm_launch_host (pinned host buffers, chunked H2D overlapped with the reduce)"
             if world == 1 else ("H2D + norm_launch_sharded + D2H of covered elements" if comm else
                                 "H2D + norm_shard_partial/all-gather/norm_shard_finish + D2H of covered elements")}

@@ -1,0 +1,64 @@
+"""bench.py's N > 1 path end to end: `torch.distributed.run --nproc-per-node 2
+bench.py --gpus 2`, the launch the driver uses for the scaling run, with both
+ranks on the one GPU of this box (gloo process group, NORM_BENCH_BACKEND=gloo:
+NCCL refuses two ranks on one device).  Checks that rank 0 prints exactly one
+JSON line with the contract's keys, that the fused peer-memory exchange was used
+(no NCCL fallback note), and that the other rank prints nothing."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _torchrun(args, timeout=600):
+    env = dict(os.environ, NORM_BENCH_BACKEND="gloo", NORM_BENCH_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2"] + args
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-4000:]
+    return json.loads(lines[0]), r
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "host"])
+def test_bench_vector_two_ranks(exchange):
+    d, r = _torchrun(["--numel", str(2**24 + 7), "--steps", "3", "--warmup", "3", "--exchange", exchange,
+                      "--e2e-steps", "1"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
+              "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
+    assert d["config"]["exchange"] == exchange
+    assert d["config"]["exchange_note"] is None, d["config"]["exchange_note"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 4 * (2**24 + 7)
+    assert "cpu_baseline" not in d or d["cpu_baseline"] is None  # rank 0 at N = 1 only
+
+
+def test_bench_rows_two_ranks():
+    d, _ = _torchrun(["--workload", "rows", "--steps", "3", "--warmup", "3"])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_bench_reference_two_ranks():
+    """--impl reference under torchrun: rank 0 alone times the oracle and prints."""
+    d, _ = _torchrun(["--impl", "reference", "--steps", "1", "--warmup", "3"])
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
