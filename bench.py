@@ -361,6 +361,37 @@ def run_vector(args, world, rank, local):
                  "note": "same-run torch streams on this rank's buffers (copy counts read+write bytes)"}
     achieved = red_bytes / (red_ms_avg / 1e3) / 1e9
     extra = {}
+    # per-step distribution (events between steps; PDL acts inside a step, so
+    # these do not perturb it) and, at N = 1, the same step replayed as a CUDA
+    # graph (norm_graph_create: reduce + scale captured with their PDL edge)
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier(world)
+    sev[0].record(stream)
+    for k in range(args.steps):
+        step()
+        sev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    per = sorted(sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps))
+    stats = {"median_ms": max_over_ranks(statistics.median(per), world),
+             "min_ms": max_over_ranks(per[0], world),
+             "p90_ms": max_over_ranks(per[min(len(per) - 1, int(0.9 * len(per)))], world)}
+    if world == 1:
+        g = L.NormGraph(out, inp, index=index, path=args.path)
+        for _ in range(2):
+            g.launch()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            g.launch()
+        b.record(stream)
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b) / args.steps
+        stats["graph_ms_per_step"] = gms
+        stats["graph_value"] = L.algorithmic_bytes(n, index) / (gms / 1e3) / 1e9
+        g.destroy()
+    extra["step_stats"] = stats
     # dense-index figure on the same buffers (caption reading R1), reported beside the headline
     if args.also_dense and index == "literal" and (world == 1 or comm is not None):
         dense_mine = L.plan_shards(n, world, "dense", True)[rank]
