@@ -341,7 +341,19 @@ def run_vector(args, world, rank, local):
     algo = L.algorithmic_bytes(n, index)
     value = algo / (ms / 1e3) / 1e9
     peak, peak_src = load_peak()
-    red_bytes = 4 * nloc  # the reduce kernel's algorithmic bytes per launch: read every owned element once
+    # the kernel the events bracket: the reduce (two-pass: 4 bytes per owned
+    # element) or, when this rank's call is one fused kernel, that kernel
+    # (4 bytes per owned element + 8 per locally covered element)
+    cov_count_g, prefix_g = L.coverage(n, index)
+    lloc = local_covered_prefix(mine, prefix_g)
+    if world == 1:
+        kpath = L.choose_path(n, prefix_g, args.path)
+    elif comm is not None and isinstance(comm, L.PeerComm):
+        kpath = L.choose_path(nloc, lloc, "auto")
+    else:
+        kpath = "two_pass"
+    fused_step = kpath == "fused"
+    red_bytes = 4 * nloc + (8 * lloc if fused_step else 0)
     # in-run calibration on the same buffers: a torch copy stream
     # (read + write bytes) and a torch read-only stream (torch.sum)
     calib = {}
@@ -415,7 +427,7 @@ def run_vector(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, world, rank, local, mine, n, index)
-    launches_per_step = 2
+    launches_per_step = 1 if fused_step else 2
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(index)
@@ -444,8 +456,10 @@ def run_vector(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
-                     "kernel": ("reduce_bulk_kernel" if nloc >= (1 << 22) else "reduce_kernel")
-                               + " (the hoisted sum: 94% of the literal step's bytes)",
+                     "kernel": ("fused_kernel (reduce + grid barrier + exchange + scale: the whole step)"
+                                if fused_step else
+                                ("reduce_bulk_kernel" if nloc >= (1 << 22) else "reduce_kernel")
+                                + " (the hoisted sum: 94% of the literal step's bytes)"),
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_instr, "instrumented_ms_per_step": ms_instr,
                      "frac_of_same_run_read_stream": (achieved / calib["torch_sum_gbs"]) if calib else None,
@@ -461,6 +475,25 @@ def run_vector(args, world, rank, local):
     print(json.dumps(line), flush=True)
     if comm:
         comm.destroy()
+
+
+def local_covered_prefix(ranges, prefix):
+    """Locally covered elements as a prefix [0, Lloc) of the local buffer, else -1
+    (mirrors comm.cpp local_covered_prefix; prefix = global L, -1 if not a prefix)."""
+    if prefix < 0:
+        return -1
+    off = lloc = 0
+    ended = False
+    for b, ln in ranges:
+        clen = max(0, min(b + ln, prefix) - b)
+        if clen > 0:
+            if ended or off != lloc:
+                return -1
+            lloc += clen
+        if clen < ln:
+            ended = True
+        off += ln
+    return lloc
 
 
 def run_e2e(args, world, rank, local, mine, n, index):

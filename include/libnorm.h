@@ -225,6 +225,13 @@ norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* p
 /* Bytes of device workspace a call with (n, o) needs if the caller supplies one. */
 norm_status_t norm_workspace_bytes(int64_t n, const norm_opts_t* o, size_t* bytes);
 
+/* The path (norm_path_t) a call takes on the CURRENT device: `requested` if not
+ * AUTO, else the AUTO rule of DESIGN.md §4 for n elements whose covered set is
+ * [0, covered_prefix) (covered_prefix = -1: not a prefix).  The sharded peer
+ * path applies it per rank to the local buffer.  Reads the device's L2 size
+ * (NORM_ERR_CUDA / NORM_ERR_UNSUPPORTED without an sm_100 device). */
+norm_status_t norm_choose_path(int64_t n, int64_t covered_prefix, int32_t requested, int32_t* chosen);
+
 /* Algorithmic HBM bytes of one call (the roofline numerator):
  * two-pass 4n + 8|C(n)|.  Pure host function. */
 norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t* bytes);
@@ -301,7 +308,13 @@ norm_status_t norm_shard_finish(float* out_local, const float* in_local, const n
  *   norm_peer_create -> 64-byte IPC handle of this rank's mailbox
  *   <caller all-gathers the W handles in rank order>
  *   norm_peer_connect(handles[W*64]) -> maps the peers' mailboxes
- * Calls on one norm_peer_t must be issued in the same order on every rank. */
+ * Calls on one norm_peer_t must be issued in the same order on every rank.
+ * o->path: AUTO applies norm_choose_path per rank to the local buffer; FUSED (or
+ * AUTO choosing it) runs ONE cooperative kernel per rank when the locally
+ * covered elements are a prefix of the local buffer: reduce, grid barrier,
+ * publish + mailbox wait, scale (the covered part read last, from L2 where it
+ * fits); TWO_PASS (or a non-prefix local coverage) runs reduce -> scale.  All
+ * give the same bits.  o->ev_reduce_* then bracket the fused kernel. */
 typedef struct norm_peer norm_peer_t;
 norm_status_t norm_peer_create(norm_peer_t** peer, int32_t world, int32_t rank,
                                unsigned char handle[64]);

@@ -22,6 +22,7 @@ from ._lib import (  # noqa: F401
     norm_bpnn_layerforward,
     norm_coverage,
     norm_algorithmic_bytes,
+    norm_choose_path,
     norm_workspace_bytes,
     norm_plan_shards,
     norm_cache_release,
@@ -31,6 +32,7 @@ from ._lib import (  # noqa: F401
     PeerComm,
     NormError,
     algorithmic_bytes,
+    choose_path,
     cache_release,
     coverage,
     last_error,
@@ -57,7 +59,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "NormGraph", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes",
+    "normalize", "normalize_form", "NormGraph", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes", "choose_path",
     "cache_release", "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

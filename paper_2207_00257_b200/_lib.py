@@ -63,6 +63,7 @@ def lib():
             "norm_coverage": [i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "norm_workspace_bytes": [i64, optp, ctypes.POINTER(ctypes.c_size_t)],
             "norm_algorithmic_bytes": [i64, i32, ctypes.POINTER(i64)],
+            "norm_choose_path": [i64, i64, i32, ctypes.POINTER(i32)],
             "norm_comm_unique_id": [ctypes.c_char_p],
             "norm_comm_init": [ctypes.POINTER(vp), i32, i32, ctypes.c_char_p],
             "norm_comm_destroy": [vp],
@@ -338,6 +339,14 @@ def algorithmic_bytes(n, index="literal"):
     return b.value
 
 
+def choose_path(n, covered_prefix, path="auto"):
+    """The path name a call over n elements with covered set [0, covered_prefix)
+    (-1: not a prefix) takes on the current device (norm_choose_path)."""
+    c = ctypes.c_int32()
+    _check(lib().norm_choose_path(n, covered_prefix, _enum(PATH, path), ctypes.byref(c)))
+    return {v: k for k, v in PATH.items()}[c.value]
+
+
 def workspace_bytes(n=0):
     b = ctypes.c_size_t()
     _check(lib().norm_workspace_bytes(n, None, ctypes.byref(b)))
@@ -460,13 +469,13 @@ class PeerComm:
         agree(st == 0, "" if st == 0 else f"norm_peer_connect: {last_error()}")
 
     def normalize_sharded(self, out_local, in_local, ranges, n_global, index="literal",
-                          stream=None, sum_out=None, sum_out_f64=None, events=None):
+                          stream=None, sum_out=None, sum_out_f64=None, events=None, path="auto"):
         _check_f32(out_local, "out_local")
         _check_f32(in_local, "in_local")
         if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
             raise ValueError("local buffers must hold exactly the shard's elements")
         shard = _shard_struct(ranges)
-        o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
+        o = _opts(index, path, stream, sum_out, sum_out_f64, events=events, device=in_local.device)
         _check(lib().norm_launch_sharded_peer(self._h, out_local.data_ptr(), in_local.data_ptr(),
                                               ctypes.byref(shard), n_global, ctypes.byref(o)))
         return out_local
@@ -513,6 +522,7 @@ norm_nll_backward = nll_backward
 norm_bpnn_layerforward = bpnn_layerforward
 norm_coverage = coverage
 norm_algorithmic_bytes = algorithmic_bytes
+norm_choose_path = choose_path
 norm_workspace_bytes = workspace_bytes
 norm_plan_shards = plan_shards
 norm_cache_release = cache_release

@@ -169,6 +169,28 @@ static norm_status_t check_shard(float* out_local, const float* in_local, const 
   return NORM_OK;
 }
 
+// The locally covered elements as a prefix [0, Lloc) of the local buffer (the
+// layout the fused kernel handles), or -1 if they are not one.  Literal mode's
+// coverage-balanced plan gives range 0 inside [0, L) and range 1 outside it, so
+// Lloc = len[0]; the one-range plan gives rank 0 the prefix.
+static int64_t local_covered_prefix(const norm_shard_t* mine, const Coverage& cov) {
+  if (cov.kind != COV_PREFIX) return -1;
+  int64_t off = 0, Lloc = 0;
+  bool ended = false;
+  for (int k = 0; k < mine->nranges; ++k) {
+    const int64_t gb = mine->begin[k], len = mine->len[k];
+    const int64_t ce = gb + len < cov.L ? gb + len : cov.L;
+    const int64_t clen = ce > gb ? ce - gb : 0;
+    if (clen > 0) {
+      if (ended || off != Lloc) return -1;
+      Lloc += clen;
+    }
+    if (clen < len) ended = true;
+    off += len;
+  }
+  return Lloc;
+}
+
 // Step 3 of the sharded path: combine the W partials in rank order (scale
 // prologue) and scale the locally covered elements of each owned range.
 static norm_status_t shard_finish(float* out_local, const float* in_local, const norm_shard_t* mine,
@@ -181,6 +203,11 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
   double* so64 = o->sum_out_f64;
   int64_t off = 0;
   bool launched = false;
+  // With the mailbox exchange the kernel before the first scale is this rank's
+  // reduce: launch the scale as its programmatic dependent (as on one GPU), so
+  // its TMA producer streams `in` while the reduce drains.  After an NCCL
+  // kernel or a caller's collective there is no such edge.
+  bool pdl = epoch != 0;
   cudaError_t e;
   for (int k = 0; k < mine->nranges; ++k) {
     const int64_t gb = mine->begin[k], len = mine->len[k];
@@ -188,8 +215,9 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
       const int64_t ce = gb + len < cov.L ? gb + len : cov.L;
       const int64_t clen = ce > gb ? ce - gb : 0;
       if (clen > 0) {
-        e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, false, st,
+        e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, pdl, st,
                          epoch);
+        pdl = false;
         if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
         so = nullptr;
         so64 = nullptr;
@@ -197,7 +225,8 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
       }
     } else if (cov.kind == COV_RESIDUE && len > 0) {
       e = launch_scale_residue(out_local + off, in_local + off, len, gb, cov.G, partials, world, so,
-                               so64, false, st, epoch);
+                               so64, pdl, st, epoch);
+      pdl = false;
       if (e != cudaSuccess) return cuda_fail(e, "scale_residue launch");
       so = nullptr;
       so64 = nullptr;
@@ -208,7 +237,7 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
   // Nothing covered here, but the caller wants s -- or the mailbox exchange needs
   // every rank to wait for every epoch (see publish_partial's parity argument).
   if (!launched && (so || so64 || epoch)) {
-    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, false, st, epoch);
+    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, pdl, st, epoch);
     if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
   }
   return NORM_OK;
@@ -383,9 +412,31 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   const unsigned long long epoch = ++p->epoch;
   Workspace ws = workspace_carve(p->ws);
+  const PeerPost post{p->peer_dev, p->rank, p->world, epoch};
+  // One fused kernel per rank (reduce, grid barrier, publish + mailbox wait,
+  // scale) when the local covered elements are a prefix of the local buffer and
+  // the per-rank AUTO rule picks it (e.g. literal 2^32 at W = 8: 2 GiB + 64 MiB
+  // covered per rank); otherwise reduce -> scale as below.  Both publish and
+  // wait once per epoch, so ranks may take different paths.
+  const Coverage gcov = coverage_of(n_global, o->index);
+  const int64_t Lloc = local_covered_prefix(mine, gcov);
+  int path = o->path;
+  if (path == NORM_PATH_AUTO) path = auto_path(local, Lloc, Lloc >= 0, d);
+  if (path == NORM_PATH_FUSED && Lloc > 0 && local > 0) {
+    Coverage lc{};
+    lc.kind = COV_PREFIX;
+    lc.n = local;
+    lc.L = lc.count = Lloc;
+    lc.G = (local + 31) / 32;
+    if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+    cudaError_t e = launch_fused(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post,
+                                 p->mail);
+    if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");
+    if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+    return NORM_OK;
+  }
   if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
-  cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st,
-                                PeerPost{p->peer_dev, p->rank, p->world, epoch});
+  cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st, post);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   return shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, epoch);

@@ -27,25 +27,36 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
 }
 
-// Single pass over HBM when the covered prefix fits in L2: one cooperative CTA
-// per SM streams the uncovered tail [L, n) through the TMA-bulk ring with an L2
-// evict_first hint, then the covered prefix [0, L) with evict_last (read LAST,
-// so it is the most recent data in L2); grid barrier; every CTA combines the
-// per-CTA partials in the same fixed order (identical s everywhere); then all
-// threads scale the prefix out of L2.  Co-residency by cooperative launch.
+// Single pass: one cooperative CTA per SM streams the uncovered
+// tail [L, n) through the TMA-bulk ring, then the covered prefix [0, L) (read
+// LAST, with an L2 evict_last hint, so as much of it as fits is still in L2);
+// grid barrier; every CTA combines the per-CTA partials in the same fixed order
+// (identical s everywhere); then every thread scales the prefix with 256-bit
+// loads (8 in flight per thread; mostly L2 hits) — measured faster here than
+// the TMA ring (profiles/r05/fused_p2.txt).  hints: 2 = also evict_first on
+// the tail (best while the prefix is small, <= L2/3), 1 = evict_last on the
+// prefix only (measured best beyond that, scripts/fused_vs_twopass.py).
+// Multi-GPU (post.mail set): after the barrier CTA 0 publishes the rank partial
+// into every rank's mailbox and every CTA waits on the local mailbox (rank-order
+// combine), so the exchange costs no extra launch.  VEC = out and in co-aligned
+// mod 32 B (else the prefix is scaled with scalar loads).
 template <bool VEC>
 __global__ void __launch_bounds__(BK_THREADS, 1)
     fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
-                 unsigned* bar, float* sum_out, double* sum_out_f64) {
+                 unsigned* bar, float* sum_out, double* sum_out_f64, int hints, PeerPost post,
+                 const double* mailbox) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
   __shared__ double red[BK_THREADS / 32];
+  __shared__ double S_sh;
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   double acc = 0.0;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
-      bulk_produce<true>(r, in + L, n - L, policy_evict_first());
-      bulk_produce<true>(r, in, L, policy_evict_last());
+      if (hints >= 2) bulk_produce<true>(r, in + L, n - L, policy_evict_first());
+      else bulk_produce<false>(r, in + L, n - L, 0);
+      if (hints >= 1) bulk_produce<true>(r, in, L, policy_evict_last());
+      else bulk_produce<false>(r, in, L, 0);
     }
   } else {
     bulk_consume(r, in + L, n - L, acc, threadIdx.x - 32);
@@ -56,7 +67,17 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   grid_barrier(bar);  // all of `in` has been read: `out` (possibly == in) may be written
   double v = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
-  const double S = block_sum(v, red);  // identical bits in every CTA
+  double S = block_sum(v, red);  // identical bits in every CTA
+  if (post.mail) {
+    if (threadIdx.x == 0) {
+      if (blockIdx.x == 0) publish_partial(post, S);
+      double Sf;
+      combine_parts(mailbox, post.world, &Sf, post.epoch);
+      S_sh = Sf;
+    }
+    __syncthreads();
+    S = S_sh;
+  }
   const float s = (float)S;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (sum_out) *sum_out = s;
@@ -65,9 +86,20 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   scale_segment<BK_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
 }
 
+// L2 hint policy (kernel comment): 2 while the covered prefix is <= L2/3, else 1.
+// NORM_FUSED_HINTS=0|1|2 overrides (A/B experiments), read once.
+static int fused_hints(const Coverage& cov, const DeviceInfo& d) {
+  static const int forced = [] {
+    const char* e = getenv("NORM_FUSED_HINTS");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced;
+  return (size_t)cov.L * 4 <= d.l2_bytes / 3 ? 2 : 1;
+}
+
 cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,
                          float* sum_out, double* sum_out_f64, const DeviceInfo& d,
-                         cudaStream_t st) {
+                         cudaStream_t st, PeerPost post, const double* mailbox) {
   const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
   void* fn = vec ? (void*)fused_kernel<true> : (void*)fused_kernel<false>;
   static int configured[64][2] = {};
@@ -84,7 +116,9 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
   int64_t n = cov.n, L = cov.L;
   double* partials = ws.partials;
   unsigned* bar = ws.bar;
-  void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64};
+  int hints = fused_hints(cov, d);
+  void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64, &hints,
+                  &post, (void*)&mailbox};
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BK_THREADS), args, BK_SMEM, st);
 }
 

@@ -238,22 +238,28 @@ static norm_status_t check_literal_grid(const Coverage& c, int index) {
 }
 
 // AUTO path thresholds, measured on B200 (scripts/small_paths.py,
-// bench.py --workload paths28):
+// scripts/fused_vs_twopass.py, profiles/r05/fused_*.txt):
 //  * n <= 2^17: one CTA does everything (3-6 us; the two-kernel path costs ~6.5 us);
-//  * fused only pays when the input does NOT fit in L2 but the covered prefix
-//    does: then the scale reads the prefix from L2 instead of HBM (literal 2^28:
-//    0.180 vs 0.187 ms).  When the whole input fits in L2 the two-pass scale hits
-//    L2 anyway and the cooperative launch + grid barrier only cost (~1 us);
+//  * fused when the input does NOT fit in L2 and only part of it is covered,
+//    with the covered bytes <= 3 x L2: one kernel instead of two saves the second
+//    launch and ramp, and the prefix read last is (partly) served from L2 —
+//    literal 2^27..2^31: 6-9 us faster per call; at 2^32 (512 MiB prefix) the
+//    fused scale phase's plain loads lose to the two-pass TMA scale (+15 us).
+//    When the whole input fits in L2 the two-pass scale hits L2 anyway and the
+//    cooperative launch + grid barrier only cost (~1 us); dense stays two-pass;
 //  * otherwise two-pass.
 constexpr int64_t kSmallN = 1 << 17;
 
-static int choose_path(const Coverage& cov, const norm_opts_t* o, const DeviceInfo& d) {
-  if (o->path != NORM_PATH_AUTO) return o->path;
-  if (cov.n <= kSmallN) return NORM_PATH_SMALL;
-  const size_t budget = d.l2_bytes / 3;  // covered bytes kept in L2 across the grid barrier
-  if (cov.kind == COV_PREFIX && (size_t)cov.n * 4 > d.l2_bytes && (size_t)cov.L * 4 <= budget)
+int auto_path(int64_t n, int64_t L, bool prefix, const DeviceInfo& d) {
+  if (n <= kSmallN) return NORM_PATH_SMALL;
+  if (prefix && L < n && (size_t)n * 4 > d.l2_bytes && (size_t)L * 4 <= 3 * d.l2_bytes)
     return NORM_PATH_FUSED;
   return NORM_PATH_TWO_PASS;
+}
+
+static int choose_path(const Coverage& cov, const norm_opts_t* o, const DeviceInfo& d) {
+  if (o->path != NORM_PATH_AUTO) return o->path;
+  return auto_path(cov.n, cov.L, cov.kind == COV_PREFIX, d);
 }
 
 static norm_status_t launch_vector(float* out, const float* in, const Coverage& cov,
@@ -468,6 +474,19 @@ struct norm_graph {
   void* ws = nullptr;
   int device = -1;
 };
+
+NORM_API norm_status_t norm_choose_path(int64_t n, int64_t covered_prefix, int32_t requested,
+                                        int32_t* chosen) {
+  if (n < 0 || !chosen || requested < NORM_PATH_AUTO || requested > NORM_PATH_SMALL ||
+      covered_prefix > n)
+    return fail(NORM_ERR_INVALID_VALUE, "bad norm_choose_path arguments");
+  DeviceInfo d;
+  norm_status_t st = check_device(&d);
+  if (st != NORM_OK) return st;
+  *chosen = requested != NORM_PATH_AUTO ? requested
+                                        : auto_path(n, covered_prefix, covered_prefix >= 0, d);
+  return NORM_OK;
+}
 
 NORM_API norm_status_t norm_graph_create(norm_graph_t** out_g, float* out, const float* in,
                                          int64_t n, const norm_opts_t* o) {

@@ -93,9 +93,12 @@ cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float
 
 // One cooperative persistent kernel: reduce (covered prefix last, L2 evict_last),
 // grid barrier, scale from L2.  Requires COV_PREFIX.
+// post.mail set: multi-GPU, the rank partial is published into every rank's
+// mailbox after the grid barrier and `mailbox` (this rank's) is waited on.
 cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,
                          float* sum_out, double* sum_out_f64, const DeviceInfo& d,
-                         cudaStream_t st);
+                         cudaStream_t st, PeerPost post = PeerPost{nullptr, 0, 0, 0},
+                         const double* mailbox = nullptr);
 
 // Batched rows: one CTA per row (grid-strided), row held in registers when it fits.
 cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
@@ -123,6 +126,10 @@ cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_
 // NEXT-4 backprop layerforward (backprop.cu)
 cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_t in, int64_t hid,
                         int variant, cudaStream_t st);
+
+// The AUTO path for a call over n elements whose covered set is [0, L) (prefix)
+// or not a prefix (libnorm.cpp; also used per rank by the sharded peer path).
+int auto_path(int64_t n, int64_t L, bool prefix, const DeviceInfo& d);
 
 // thread-local error detail
 void set_error(const std::string& s);

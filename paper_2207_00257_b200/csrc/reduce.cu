@@ -10,20 +10,6 @@
 
 namespace lnorm {
 
-// Fused exchange: the rank's partial goes straight from the reduce's last CTA into
-// slot [epoch & 1][rank] of every rank's mailbox (peer stores through NVLink),
-// then one system-scope fence and the epoch flags (release).  Parity double
-// buffering makes a fast rank's next epoch unable to overwrite a slot that a slow
-// rank has not read yet (the next epoch's reduce needs this epoch's scale done).
-__device__ __forceinline__ void publish_partial(const PeerPost& post, double S) {
-  if (!post.mail) return;
-  const size_t slot = ((size_t)(post.epoch & 1) * post.world + post.rank) * 2;
-  for (int r = 0; r < post.world; ++r) st_relaxed_sys_f64(post.mail[r] + slot, S);
-  __threadfence_system();
-  for (int r = 0; r < post.world; ++r)
-    st_release_sys_u64(reinterpret_cast<unsigned long long*>(post.mail[r] + slot + 1), post.epoch);
-}
-
 // --------------------------------------------------------------- reduce
 // Pass 1 of the two-pass path: S = sum in[0, n).  Persistent grid (2 CTAs/SM),
 // per-CTA partial, last-CTA ticket combines the partials in index order.

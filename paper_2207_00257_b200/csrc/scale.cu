@@ -10,35 +10,6 @@
 
 namespace lnorm {
 
-__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full,
-                                              unsigned long long epoch = 0) {
-  double S;
-  if (epoch == 0) {
-    S = __ldcg(S_parts);
-    for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
-  } else {
-    // mailbox: wait for every rank's slot of this epoch (peer stores over NVLink)
-    const double* box = S_parts + (size_t)(epoch & 1) * nparts * 2;
-    const unsigned long long t0 = globaltimer_ns();
-    bool ok = true;
-    for (int r = 0; r < nparts && ok; ++r) {
-      const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(box + 2 * r + 1);
-      while (ld_acquire_sys_u64(flag) != epoch) {
-        if (globaltimer_ns() - t0 > 30000000000ull) { ok = false; break; }  // peer lost: no hang
-        __nanosleep(64);
-      }
-    }
-    if (!ok) {
-      S = __longlong_as_double(0x7ff8000000000000ll);
-    } else {
-      S = ld_relaxed_sys_f64(box);
-      for (int r = 1; r < nparts; ++r) S += ld_relaxed_sys_f64(box + 2 * r);  // rank order
-    }
-  }
-  *S_full = S;
-  return (float)S;  // RN to binary32
-}
-
 // ---------------------------------------------------------------- scale
 template <bool VEC, bool ALIAS>
 __global__ void __launch_bounds__(SC_THREADS)
@@ -90,34 +61,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
-  const float s = s_sh;
-  const Divisor dv = make_divisor(s);
-  constexpr int64_t CF = SB_CHUNK / 4;
-  int64_t head, nchunks;
-  bulk_split<CF>(in, len, &head, &nchunks);
-  float* ob = out + head;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    mbar_wait(&r.full[r.stage], r.phase);
-    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * SB_CHUNK);
-    float* oc = ob + c * CF;
-#pragma unroll
-    for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
-      const int i = k * BK_CONSUMERS + ct;
-      const float4 a = q[2 * i], b = q[2 * i + 1];
-#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
-      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
-#else
-      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
-#endif
-    }
-    stage_release(&r.empty[r.stage]);
-    r.advance();
-  }
-  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
-  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
-       i += (int64_t)gridDim.x * BK_CONSUMERS)
-    out[i] = div_rn(in[i], dv);
-  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
+  bulk_scale_consume(r, out, in, len, make_divisor(s_sh), ct);
 }
 
 __global__ void __launch_bounds__(256)

@@ -152,24 +152,45 @@ __device__ __forceinline__ void bulk_split(const float* p, int64_t len, int64_t*
   *nchunks = (len - h) / CF;
 }
 
+// Producer cursor over this CTA's chunks of a segment [p, p + len): chunk c of
+// the 32-byte-aligned body, c = blockIdx.x, blockIdx.x + gridDim.x, ...  Lets a
+// kernel issue part of a segment (e.g. prefetch the first stages of a later
+// phase) and resume it later; bulk_produce issues it all.
+struct BulkCursor {
+  const float* body;
+  int64_t c, nchunks;
+};
+
+template <int64_t CF>
+__device__ __forceinline__ BulkCursor bulk_cursor(const float* p, int64_t len) {
+  if (len <= 0) return BulkCursor{p, 0, 0};
+  int64_t head, nchunks;
+  bulk_split<CF>(p, len, &head, &nchunks);
+  return BulkCursor{p + head, (int64_t)blockIdx.x, nchunks};
+}
+
+// Issue up to max_issue of the cursor's remaining chunks (call from one lane).
+template <bool HINT, int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_issue(BulkRing<STAGES, CHUNK>& r, BulkCursor& cur, int64_t max_issue,
+                                           uint64_t pol) {
+  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
+  for (int64_t k = 0; k < max_issue && cur.c < cur.nchunks; ++k, cur.c += gridDim.x) {
+    if (r.issued >= STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+    mbar_arrive_expect_tx(&r.full[r.stage], CHUNK);
+    void* dst = r.buf + (size_t)r.stage * CHUNK;
+    if (HINT) bulk_g2s_hint(dst, cur.body + cur.c * CF, CHUNK, &r.full[r.stage], pol);
+    else bulk_g2s(dst, cur.body + cur.c * CF, CHUNK, &r.full[r.stage]);
+    ++r.issued;
+    r.advance();
+  }
+}
+
 // Producer side (call from one lane): issue this CTA's chunks of [p, p + len).
 template <bool HINT, int STAGES, int CHUNK>
 __device__ __forceinline__ void bulk_produce(BulkRing<STAGES, CHUNK>& r, const float* p, int64_t len,
                                              uint64_t pol) {
-  if (len <= 0) return;
-  constexpr int64_t CF = BulkRing<STAGES, CHUNK>::CF;
-  int64_t head, nchunks;
-  bulk_split<CF>(p, len, &head, &nchunks);
-  const float* body = p + head;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    if (r.issued >= STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
-    mbar_arrive_expect_tx(&r.full[r.stage], CHUNK);
-    void* dst = r.buf + (size_t)r.stage * CHUNK;
-    if (HINT) bulk_g2s_hint(dst, body + c * CF, CHUNK, &r.full[r.stage], pol);
-    else bulk_g2s(dst, body + c * CF, CHUNK, &r.full[r.stage]);
-    ++r.issued;
-    r.advance();
-  }
+  BulkCursor cur = bulk_cursor<BulkRing<STAGES, CHUNK>::CF>(p, len);
+  bulk_issue<HINT>(r, cur, INT64_MAX, pol);
 }
 
 // Consumer side (warps 1..8, ct = consumer thread index): acc += this CTA's share.
@@ -201,6 +222,45 @@ __device__ __forceinline__ void bulk_consume(BulkRing<STAGES, CHUNK>& r, const f
   if (blockIdx.x == 0 && ct < head) acc += (double)p[ct];
 }
 
+// Consumer side of a scale stream (warps 1..8): out[i] = in[i] / s for this CTA's
+// chunks of [in, in + len), read from the ring, stored with STG.E.256 (.cs);
+// out must be co-aligned with in mod 32 B.  The remainder and the head go through
+// plain loads, each element read and written by the same thread (so out may
+// alias in: every chunk is loaded into shared memory before this CTA, its only
+// writer, stores over it).
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ void bulk_scale_consume(BulkRing<STAGES, CHUNK>& r, float* out, const float* in,
+                                                   int64_t len, const Divisor& dv, int ct) {
+  if (len <= 0) return;
+  constexpr int64_t CF = CHUNK / 4;
+  static_assert(CHUNK % (32 * BK_CONSUMERS) == 0, "whole 8-float groups per consumer");
+  int64_t head, nchunks;
+  bulk_split<CF>(in, len, &head, &nchunks);
+  float* ob = out + head;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * CHUNK);
+    float* oc = ob + c * CF;
+#pragma unroll
+    for (int k = 0; k < CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+#if defined(NORM_AB_SCALE_DIV8)  // A/B experiments only
+      st8_stream(oc + (int64_t)i * 8, div8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#else
+      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+#endif
+    }
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    out[i] = div_rn(in[i], dv);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
+}
+
 template <int STAGES, int CHUNK>
 __device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char* buf, uint64_t* full,
                                                                   uint64_t* empty) {
@@ -213,6 +273,54 @@ __device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char*
   }
   __syncthreads();
   return BulkRing<STAGES, CHUNK>{buf, full, empty, 0, 0u, 0};
+}
+
+// ---- rank partials (multi-GPU) ---------------------------------------------
+// Fused exchange: the rank's partial goes straight from the reduce's last CTA into
+// slot [epoch & 1][rank] of every rank's mailbox (peer stores through NVLink),
+// then one system-scope fence and the epoch flags (release).  Parity double
+// buffering makes a fast rank's next epoch unable to overwrite a slot that a slow
+// rank has not read yet (the next epoch's reduce needs this epoch's scale done).
+__device__ __forceinline__ void publish_partial(const PeerPost& post, double S) {
+  if (!post.mail) return;
+  const size_t slot = ((size_t)(post.epoch & 1) * post.world + post.rank) * 2;
+  for (int r = 0; r < post.world; ++r) st_relaxed_sys_f64(post.mail[r] + slot, S);
+  __threadfence_system();
+  for (int r = 0; r < post.world; ++r)
+    st_release_sys_u64(reinterpret_cast<unsigned long long*>(post.mail[r] + slot + 1), post.epoch);
+}
+
+// s = (float)(S_parts[0] + ... + S_parts[nparts-1]) in that fixed order; with
+// epoch != 0, S_parts is this rank's mailbox: wait (acquire, system scope, ~30 s
+// timeout -> NaN) for every slot of parity epoch & 1 to carry `epoch`, then
+// combine the slots in rank order.  *S_full receives the fp64 sum.
+__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full,
+                                              unsigned long long epoch = 0) {
+  double S;
+  if (epoch == 0) {
+    S = __ldcg(S_parts);
+    for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
+  } else {
+    // mailbox: wait for every rank's slot of this epoch (peer stores over NVLink)
+    const double* box = S_parts + (size_t)(epoch & 1) * nparts * 2;
+    const unsigned long long t0 = globaltimer_ns();
+    bool ok = true;
+    for (int r = 0; r < nparts && ok; ++r) {
+      const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(box + 2 * r + 1);
+      while (ld_acquire_sys_u64(flag) != epoch) {
+        if (globaltimer_ns() - t0 > 30000000000ull) { ok = false; break; }  // peer lost: no hang
+        __nanosleep(64);
+      }
+    }
+    if (!ok) {
+      S = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      S = ld_relaxed_sys_f64(box);
+      for (int r = 1; r < nparts; ++r) S += ld_relaxed_sys_f64(box + 2 * r);  // rank order
+    }
+  }
+  *S_full = S;
+  return (float)S;  // RN to binary32
 }
 
 template <typename Kern, typename... Args>

@@ -37,9 +37,9 @@ def _torchrun(args, timeout=600):
     return json.loads(lines[0]), r
 
 
-@pytest.mark.parametrize("exchange", ["p2p", "host"])
-def test_bench_vector_two_ranks(exchange):
-    d, r = _torchrun(["--numel", str(2**24 + 7), "--steps", "3", "--warmup", "3", "--exchange", exchange,
+@pytest.mark.parametrize("exchange,n", [("p2p", 2**24 + 7), ("host", 2**24 + 7), ("p2p", 2**27 + 7)])
+def test_bench_vector_two_ranks(exchange, n):
+    d, r = _torchrun(["--numel", str(n), "--steps", "3", "--warmup", "3", "--exchange", exchange,
                       "--e2e-steps", "1"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
@@ -48,7 +48,10 @@ def test_bench_vector_two_ranks(exchange):
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
     assert d["config"]["exchange"] == exchange
     assert d["config"]["exchange_note"] is None, d["config"]["exchange_note"]
-    assert d["e2e"]["h2d_bytes_per_step"] == 4 * (2**24 + 7)
+    assert d["e2e"]["h2d_bytes_per_step"] == 4 * n
+    # each rank's local input exceeds L2 at 2^27: the peer path runs one fused kernel per rank
+    assert ("fused_kernel" in d["roofline"]["kernel"]) == (exchange == "p2p" and n > 2**26)
+    assert d["gpu_launches"] == d["steps"] * (1 if "fused_kernel" in d["roofline"]["kernel"] else 2)
     assert "cpu_baseline" not in d or d["cpu_baseline"] is None  # rank 0 at N = 1 only
 
 

@@ -56,9 +56,10 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
             ref = torch.full((nloc,), -5.0, device="cuda")
             sref = torch.zeros(1, device="cuda")
             L.normalize_sharded_via(ref, inp, ranges, n, ag, index=mode, sum_out=sref)
+            path = "fused" if exchange == "peer-fused" else ("two_pass" if exchange == "peer-2p" else "auto")
             for _ in range(7):
                 out.fill_(-5.0)
-                pc.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s)
+                pc.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s, path=path)
                 torch.cuda.synchronize()
                 assert torch.equal(out, ref) and torch.equal(s, sref)
             dist.barrier()
@@ -77,6 +78,12 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
     (2, 2**22 + 7, "literal", True, "peer"),
     (4, 3 * 2**20 + 5, "dense", True, "peer"),
     (3, 700, "literal", True, "peer"),  # ranks without covered elements still wait every epoch
+    # one fused kernel per rank (reduce, grid barrier, publish + mailbox wait, scale)
+    (2, 2**22 + 7, "literal", True, "peer-fused"),
+    (3, 3 * 2**20 + 5, "dense", True, "peer-fused"),
+    (2, 2**20 + 7, "literal", False, "peer-fused"),  # one-range plan: rank 1 has nothing covered
+    (2, 2**26 + 7, "literal", True, "peer"),  # AUTO picks fused per rank (local input > L2)
+    (2, 2**26 + 7, "literal", True, "peer-2p"),
 ])
 def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange):
     import gen

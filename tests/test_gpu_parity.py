@@ -599,3 +599,38 @@ def test_graph_plan_matches_eager(n, mode, path):
     assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
     check(x.cpu().numpy(), out.cpu().numpy(), np.float32(s.item()), mode, 0)
     g.destroy()
+
+
+@pytest.mark.parametrize("n", [2**29 + 3, 2**31 - 5])
+def test_auto_fused_literal_mid_sizes(n):
+    """AUTO takes the fused kernel for literal inputs larger than L2 whose covered
+    prefix is <= 3 x L2: every covered element replayed bitwise,
+    s against the oracle's exact sum, sampled uncovered sentinels."""
+    count, prefix = L.coverage(n, "literal")
+    assert L.choose_path(n, prefix) == "fused"
+    assert L.choose_path(n, prefix, "two_pass") == "two_pass"
+    assert L.choose_path(2**32, L.coverage(2**32)[1]) == "two_pass"
+    assert L.choose_path(2**28, -1) == "two_pass"  # dense-like / non-prefix coverage
+    inp = torch.empty(n, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(inp, seed=5, dist=0)
+    out = torch.empty(n, dtype=torch.int32, device="cuda").fill_(SENTINEL_BITS).view(torch.float32)
+    s = torch.zeros(1, device="cuda")
+    L.normalize(out, inp, index="literal", sum_out=s)
+    torch.cuda.synchronize()
+    x = inp.cpu().numpy()
+    S = oracle.sum_exact(x)
+    sv = np.float32(s.item())
+    assert abs(float(sv) - S) <= 1e-6 * S
+    o = out[:prefix].cpu().numpy()
+    assert np.array_equal(o, x[:prefix] / sv)
+    ref = x[:prefix].astype(np.float64) / S
+    assert np.max(np.abs(o - ref) / ref) <= 1e-5
+    idx = torch.from_numpy(np.random.default_rng(3).integers(prefix, n, 1 << 20)).cuda()
+    assert torch.all(out.view(torch.int32)[idx] == SENTINEL_BITS)
+    # same bits as the two-pass path? not required (different partition); but the
+    # fused result must be repeatable bit for bit
+    out2 = torch.empty_like(out).view(torch.int32).fill_(SENTINEL_BITS).view(torch.float32)
+    s2 = torch.zeros(1, device="cuda")
+    L.normalize(out2, inp, index="literal", sum_out=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(s, s2) and torch.equal(out[:prefix], out2[:prefix])
