@@ -313,8 +313,10 @@ norm_status_t norm_shard_finish(float* out_local, const float* in_local, const n
  * AUTO choosing it) runs ONE cooperative kernel per rank when the locally
  * covered elements are a prefix of the local buffer: reduce, grid barrier,
  * publish + mailbox wait, scale (the covered part read last, from L2 where it
- * fits); TWO_PASS (or a non-prefix local coverage) runs reduce -> scale.  All
- * give the same bits.  o->ev_reduce_* then bracket the fused kernel. */
+ * fits); TWO_PASS (or a non-prefix local coverage) runs reduce -> scale.  Each
+ * path is deterministic; their local partials differ only in summation order
+ * (bit-identical whenever the fp64 accumulation is exact, e.g. grid-valued
+ * inputs).  o->ev_reduce_* bracket the fused kernel when it runs. */
 typedef struct norm_peer norm_peer_t;
 norm_status_t norm_peer_create(norm_peer_t** peer, int32_t world, int32_t rank,
                                unsigned char handle[64]);
