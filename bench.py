@@ -458,7 +458,8 @@ def run_vector(args, world, rank, local):
                      "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
                      "kernel": ("fused_kernel (reduce + grid barrier + exchange + scale: the whole step)"
                                 if fused_step else
-                                ("reduce_bulk_kernel" if nloc >= (1 << 22) else "reduce_kernel")
+                                ("reduce_dyn_kernel (TMA-bulk reduce, dynamic deterministic tail)"
+                                 if nloc >= (1 << 22) else "reduce_kernel")
                                 + " (the hoisted sum: 94% of the literal step's bytes)"),
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_instr, "instrumented_ms_per_step": ms_instr,

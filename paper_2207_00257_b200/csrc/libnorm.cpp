@@ -127,7 +127,8 @@ static norm_status_t check_device(DeviceInfo* d) {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 size_t workspace_bytes() {
-  return align_up(kMaxGrid * sizeof(double), 256) + 256 /* S[4] */ + 256 /* ticket, bar */;
+  return align_up(kMaxGrid * sizeof(double), 256) + 256 /* S[4] */ + 256 /* ticket, bar, task_ctr */ +
+         align_up(kMaxTasks * sizeof(double), 256);
 }
 
 Workspace workspace_carve(void* base) {
@@ -139,6 +140,9 @@ Workspace workspace_carve(void* base) {
   p += 256;
   w.ticket = reinterpret_cast<unsigned*>(p);
   w.bar = w.ticket + 1;
+  w.task_ctr = w.ticket + 4;
+  p += 256;
+  w.task_sums = reinterpret_cast<double*>(p);
   return w;
 }
 

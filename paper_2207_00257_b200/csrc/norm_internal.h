@@ -25,12 +25,15 @@ Coverage coverage_of(int64_t n, int index);
 // Device workspace (one per (device, stream) in the internal cache, or carved
 // from the caller's buffer).  Must be zero-filled before first use; every
 // kernel that uses the counters returns them to zero.
-constexpr int kMaxGrid = 4096;  // max CTAs of any persistent reduce grid
+constexpr int kMaxGrid = 4096;   // max CTAs of any persistent reduce grid
+constexpr int kMaxTasks = 16384; // max dynamically scheduled tasks of the bulk reduce
 struct Workspace {
-  double* partials;  // [kMaxGrid] per-CTA partial sums
-  double* S;         // [4] fp64 sum slots (S[0]: vector sum; S[1]: sharded local partial)
-  unsigned* ticket;  // [1] last-block ticket of the reduce kernel
-  unsigned* bar;     // [2] grid barrier {count, generation} of the fused kernel
+  double* partials;    // [kMaxGrid] per-CTA partial sums
+  double* S;           // [4] fp64 sum slots (S[0]: vector sum; S[1]: sharded local partial)
+  unsigned* ticket;    // [1] last-block ticket of the reduce kernel
+  unsigned* bar;       // [2] grid barrier {count, generation} of the fused kernel
+  unsigned* task_ctr;  // [1] next task of the bulk reduce's dynamic tail
+  double* task_sums;   // [kMaxTasks] per-task sums of the dynamic tail
 };
 size_t workspace_bytes();
 Workspace workspace_carve(void* base);

@@ -82,6 +82,147 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
 }
 
+// Pass 1, TMA-bulk with a dynamically scheduled, still deterministic tail.
+// Measured (scripts/reduce_timeline.cu): with every chunk dealt statically the
+// per-SM streaming rates differ by ~1-2 % at random, so the last CTA finishes
+// ~20-40 us after the median at n = 2^32 (~6 us at 2^29) while the others idle.
+// Here the first nchunks - dyn chunks are dealt grid-strided as in
+// reduce_bulk_kernel (one partial per CTA), and the last `dyn` chunks form tasks
+// of `tc` consecutive chunks that CTAs claim with an atomic counter as they run
+// dry.  Determinism does not depend on who runs a task: a task's sum is formed
+// in a fixed order (each consumer thread over its groups of the task's chunks in
+// chunk order, warp butterfly, then the 8 warp sums in warp order by whichever
+// warp finishes the task last) and stored in task_sums[t]; the last CTA adds the
+// per-CTA partials and then the task sums in index order.  tc >= BK_STAGES, so a
+// warp can be at most one task ahead of another (double-buffered task slots).
+constexpr int kDynMinTC = BK_STAGES;
+
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    reduce_dyn_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
+                      unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
+                      PeerPost post, unsigned* __restrict__ task_ctr, double* __restrict__ task_sums,
+                      int64_t dyn, int tc) {
+  if (early_trigger) pdl_launch_dependents();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ int64_t stage_chunk[BK_STAGES];  // dynamic part: chunk index in flight, -1 = no more
+  __shared__ double red[BK_THREADS / 32];
+  __shared__ double slot[2][BK_CONSUMERS / 32];
+  __shared__ unsigned slot_cnt[2];
+  __shared__ unsigned is_last;
+  if (threadIdx.x < 2) slot_cnt[threadIdx.x] = 0u;
+  auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
+  constexpr int64_t CF = BulkRing<BK_STAGES, BK_CHUNK>::CF;
+  int64_t head, nchunks;
+  bulk_split<CF>(in, n, &head, &nchunks);
+  const float* body = in + head;
+  if (dyn > nchunks) dyn = nchunks;
+  const int64_t ns = nchunks - dyn;                // static chunks [0, ns)
+  const int64_t ntasks = (dyn + tc - 1) / tc;      // dynamic chunks [ns, nchunks)
+  double acc = 0.0;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      BulkCursor cur{body, (int64_t)blockIdx.x, ns};
+      bulk_issue<false>(r, cur, INT64_MAX, 0);
+      // claim one task ahead, so the atomic's round trip overlaps a task's loads
+      int64_t next = ntasks > 0 ? (int64_t)atomicAdd(task_ctr, 1u) : ntasks;
+      for (;;) {
+        const int64_t t = next;
+        if (t < ntasks) next = (int64_t)atomicAdd(task_ctr, 1u);
+        const int64_t c0 = ns + t * tc, c1 = t < ntasks ? (c0 + tc < nchunks ? c0 + tc : nchunks) : c0;
+        for (int64_t c = c0; c < c1; ++c) {
+          if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+          stage_chunk[r.stage] = c;
+          mbar_arrive_expect_tx(&r.full[r.stage], BK_CHUNK);
+          bulk_g2s(r.buf + (size_t)r.stage * BK_CHUNK, body + c * CF, BK_CHUNK, &r.full[r.stage]);
+          ++r.issued;
+          r.advance();
+        }
+        if (t >= ntasks) break;
+      }
+      // end marker: a stage whose full barrier completes with no bytes
+      if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+      stage_chunk[r.stage] = -1;
+      mbar_arrive(&r.full[r.stage]);
+    }
+  } else {
+    const int ct = threadIdx.x - 32, w = ct >> 5, lane = ct & 31;
+    for (int64_t c = blockIdx.x; c < ns; c += gridDim.x) {  // static part, as bulk_consume
+      mbar_wait(&r.full[r.stage], r.phase);
+      const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
+#pragma unroll
+      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+        const int i = k * BK_CONSUMERS + ct;
+        const float4 a = q[2 * i], b = q[2 * i + 1];
+        acc += sum8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}});
+      }
+      stage_release(&r.empty[r.stage]);
+      r.advance();
+    }
+    double tacc = 0.0;
+    unsigned done = 0;  // tasks finished by this warp (same sequence in every warp)
+    for (;;) {
+      mbar_wait(&r.full[r.stage], r.phase);
+      const int64_t c = *(volatile int64_t*)&stage_chunk[r.stage];
+      if (c < 0) break;
+      const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
+#pragma unroll
+      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+        const int i = k * BK_CONSUMERS + ct;
+        const float4 a = q[2 * i], b = q[2 * i + 1];
+        tacc += sum8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}});
+      }
+      stage_release(&r.empty[r.stage]);
+      r.advance();
+      const int64_t d = c - ns;
+      if ((d + 1) % tc == 0 || c + 1 == nchunks) {  // last chunk of task d / tc
+        const double v = warp_sum(tacc);
+        tacc = 0.0;
+        const unsigned p = done++ & 1u;
+        if (lane == 0) {
+          slot[p][w] = v;
+          __threadfence_block();
+          if (atomicAdd(&slot_cnt[p], 1u) == BK_CONSUMERS / 32 - 1) {
+            __threadfence_block();
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < BK_CONSUMERS / 32; ++k) t += *(volatile double*)&slot[p][k];
+            task_sums[d / tc] = t;
+            __threadfence();  // before this CTA's ticket: the last CTA reads task_sums
+            slot_cnt[p] = 0u;
+          }
+        }
+      }
+    }
+    // remainder (< one chunk) and head: plain loads into the static partial
+    const int64_t rbeg = head + nchunks * CF;
+    for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < n;
+         i += (int64_t)gridDim.x * BK_CONSUMERS)
+      acc += (double)in[i];
+    if (blockIdx.x == 0 && ct < head) acc += (double)in[ct];
+  }
+  if (!early_trigger) pdl_launch_dependents();
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
+  for (int64_t t = threadIdx.x; t < ntasks; t += BK_THREADS) v += __ldcg(task_sums + t);
+  const double S = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    *S_out = S;
+    *ticket = 0u;
+    *task_ctr = 0u;
+    publish_partial(post, S);
+  }
+}
+
 int reduce_grid(const DeviceInfo& d, int64_t n) {
   const int64_t chunks = (n / 8 + (int64_t)RED_THREADS * RED_UNROLL - 1) / ((int64_t)RED_THREADS * RED_UNROLL);
   int64_t g = (int64_t)d.sms * RED_CTAS_PER_SM;
@@ -103,6 +244,28 @@ int pdl_mode() {
   return mode;
 }
 
+// Dynamic tail of the bulk reduce: `frac` of the chunks (NORM_DYN_PCT percent,
+// default kDynPct; 0 = fully static reduce_bulk_kernel) in tasks of tc chunks
+// (NORM_DYN_TC, default kDynTC, >= BK_STAGES), capped at kMaxTasks tasks.
+constexpr int kDynPct = 3, kDynTC = 8;  // profiles/r05/dyn_sweep2.txt
+
+static int64_t dyn_chunks(int64_t n, int* tc_out) {
+  static const int pct = [] {
+    const char* e = getenv("NORM_DYN_PCT");
+    return e ? atoi(e) : kDynPct;
+  }();
+  static const int tc = [] {
+    const char* e = getenv("NORM_DYN_TC");
+    const int v = e ? atoi(e) : kDynTC;
+    return v < kDynMinTC ? kDynMinTC : v;
+  }();
+  *tc_out = tc;
+  const int64_t nchunks = n / (BK_CHUNK / 4);
+  int64_t dyn = nchunks * pct / 100;
+  if (dyn > (int64_t)kMaxTasks * tc) dyn = (int64_t)kMaxTasks * tc;
+  return pct > 0 ? dyn : 0;
+}
+
 cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, double* S_out,
                           const DeviceInfo& d, cudaStream_t st, PeerPost post) {
 #if defined(NORM_FAULT) && NORM_FAULT == 1  // fault (tests only): the sum drops the last element
@@ -116,6 +279,21 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
                                            (int)smem);
       if (e != cudaSuccess) return e;
       configured[d.device] = 1;
+    }
+    int tc = 0;
+    const int64_t dyn = dyn_chunks(n, &tc);
+    if (dyn > 0) {
+      static int configured_dyn[64] = {0};
+      if (d.device < 64 && !configured_dyn[d.device]) {
+        cudaError_t e = cudaFuncSetAttribute(reduce_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured_dyn[d.device] = 1;
+      }
+      reduce_dyn_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
+                                                         pdl_mode() == PDL_EARLY, post, ws.task_ctr,
+                                                         ws.task_sums, dyn, tc);
+      return cudaGetLastError();
     }
     reduce_bulk_kernel<<<d.sms, BK_THREADS, smem, st>>>(in, n, ws.partials, ws.ticket, S_out,
                                                         pdl_mode() == PDL_EARLY, post);

@@ -9,7 +9,7 @@ mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/${TAG}_launches_vector.csv \
     python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > $OUT/${TAG}_launches_vector.bench.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:reduce_bulk_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"reduce_dyn_kernel|reduce_bulk_kernel" -s 3 -c 1 \
     -o $OUT/${TAG}_reduce python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:scale_bulk_kernel -s 3 -c 1 \
     -o $OUT/${TAG}_scale python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1

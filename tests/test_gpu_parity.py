@@ -634,3 +634,28 @@ def test_auto_fused_literal_mid_sizes(n):
     L.normalize(out2, inp, index="literal", sum_out=s2)
     torch.cuda.synchronize()
     assert torch.equal(s, s2) and torch.equal(out[:prefix], out2[:prefix])
+
+
+@pytest.mark.parametrize("offset", [0, 3])
+def test_dynamic_tail_deterministic(offset):
+    """The bulk reduce hands its last chunks out dynamically (whichever CTA runs
+    dry first takes the next task); the sum must not depend on who ran what.
+    Wide-exponent inputs (D4) make any change of summation order visible in the
+    fp64 bits of S; 12 repeats, literal and dense, misaligned base included."""
+    n = 2**26 + 77
+    x = torch.empty(n + offset, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(x, seed=17, dist=4)
+    inp = x[offset:]
+    ref = None
+    for _ in range(12):
+        for mode in ("literal", "dense"):
+            out = torch.empty_like(inp)
+            S = torch.zeros(1, dtype=torch.float64, device="cuda")
+            L.normalize(out, inp, index=mode, path="two_pass", sum_out_f64=S)
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = S.item()
+                xs = inp.cpu().numpy()
+                Sx = oracle.sum_exact(xs)
+                assert abs(ref - Sx) <= 1e-6 * oracle.sum_abs_exact(xs)
+            assert S.item() == ref
