@@ -195,7 +195,7 @@ static int64_t local_covered_prefix(const norm_shard_t* mine, const Coverage& co
 // prologue) and scale the locally covered elements of each owned range.
 static norm_status_t shard_finish(float* out_local, const float* in_local, const norm_shard_t* mine,
                                   int64_t n_global, const double* partials, int world,
-                                  const norm_opts_t* o, const DeviceInfo& d,
+                                  const norm_opts_t* o, const DeviceInfo& d, const Workspace& ws,
                                   unsigned long long epoch = 0) {
   const Coverage cov = coverage_of(n_global, o->index);
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
@@ -216,7 +216,7 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
       const int64_t clen = ce > gb ? ce - gb : 0;
       if (clen > 0) {
         e = launch_scale(out_local + off, in_local + off, clen, partials, world, so, so64, d, pdl, st,
-                         epoch);
+                         epoch, ws.scale_ctr);
         pdl = false;
         if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
         so = nullptr;
@@ -237,7 +237,7 @@ static norm_status_t shard_finish(float* out_local, const float* in_local, const
   // Nothing covered here, but the caller wants s -- or the mailbox exchange needs
   // every rank to wait for every epoch (see publish_partial's parity argument).
   if (!launched && (so || so64 || epoch)) {
-    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, pdl, st, epoch);
+    e = launch_scale(out_local, in_local, 0, partials, world, so, so64, d, pdl, st, epoch, ws.scale_ctr);
     if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
   }
   return NORM_OK;
@@ -267,12 +267,12 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
   if (c->mode == NORM_COMM_ALLREDUCE) {  // NCCL's own summation order; one partial back
     ncclResult_t r = ncclAllReduce(c->send, c->recv, 1, ncclFloat64, ncclSum, c->nccl, st);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
-    return shard_finish(out_local, in_local, mine, n_global, c->recv, 1, o, d);
+    return shard_finish(out_local, in_local, mine, n_global, c->recv, 1, o, d, ws);
   }
   ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
   // 3. rank-order combine + scale
-  return shard_finish(out_local, in_local, mine, n_global, c->recv, c->world, o, d);
+  return shard_finish(out_local, in_local, mine, n_global, c->recv, c->world, o, d, ws);
 }
 
 NORM_API norm_status_t norm_shard_partial(double* partial, const float* in_local, int64_t n_local,
@@ -310,7 +310,10 @@ NORM_API norm_status_t norm_shard_finish(float* out_local, const float* in_local
   DeviceInfo d;
   std::string err;
   if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
-  return shard_finish(out_local, in_local, mine, n_global, partials, world, o, d);
+  Workspace ws;
+  s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws);
+  if (s != NORM_OK) return s;
+  return shard_finish(out_local, in_local, mine, n_global, partials, world, o, d, ws);
 }
 
 // ======================================================= fused peer exchange
@@ -439,5 +442,5 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
   cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st, post);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
-  return shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, epoch);
+  return shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, ws, epoch);
 }

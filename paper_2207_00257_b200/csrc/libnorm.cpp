@@ -141,6 +141,7 @@ Workspace workspace_carve(void* base) {
   w.ticket = reinterpret_cast<unsigned*>(p);
   w.bar = w.ticket + 1;
   w.task_ctr = w.ticket + 4;
+  w.scale_ctr = w.ticket + 6;
   p += 256;
   w.task_sums = reinterpret_cast<double*>(p);
   return w;
@@ -288,7 +289,7 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
   if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
   if (cov.kind == COV_PREFIX)
-    e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st);
+    e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st, 0, ws.scale_ctr);
   else
     e = launch_scale_residue(out, in, cov.n, 0, cov.G, ws.S, 1, o->sum_out, o->sum_out_f64, true, st);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "scale_kernel launch");
@@ -422,7 +423,7 @@ static norm_status_t launch_host(float* out_host, const float* in_host, const Co
   const int nparts = (int)chunks.size();
   if (cov.kind == COV_PREFIX) {
     e = launch_scale(h->resident, h->resident, cov.L, h->chunkS, nparts, o->sum_out,
-                     o->sum_out_f64, d, false, st);
+                     o->sum_out_f64, d, false, st, 0, ws.scale_ctr);
     if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
     e = cudaMemcpyAsync(out_host, h->resident, (size_t)cov.L * 4, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");

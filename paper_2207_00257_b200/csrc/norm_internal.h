@@ -33,6 +33,7 @@ struct Workspace {
   unsigned* ticket;    // [1] last-block ticket of the reduce kernel
   unsigned* bar;       // [2] grid barrier {count, generation} of the fused kernel
   unsigned* task_ctr;  // [1] next task of the bulk reduce's dynamic tail
+  unsigned* scale_ctr; // [2] {next chunk, producers done} of the bulk scale's chunk queue
   double* task_sums;   // [kMaxTasks] per-task sums of the dynamic tail
 };
 size_t workspace_bytes();
@@ -78,10 +79,12 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
 // epoch != 0: S_parts is this rank's mailbox; the prologue waits (acquire, system
 // scope, ~30 s timeout -> NaN) until all nparts slots of parity epoch & 1 carry
 // `epoch`, then combines them in rank order.
+// ctr (Workspace::scale_ctr, zeroed; left zeroed): the bulk kernel deals its
+// chunks from a queue instead of grid-strided (NULL: grid-strided).
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64,
                          const DeviceInfo& d, bool pdl, cudaStream_t st,
-                         unsigned long long epoch = 0);
+                         unsigned long long epoch = 0, unsigned* ctr = nullptr);
 
 // Residue coverage (literal, G < 32): local element j is global index gbegin + j;
 // written iff (gbegin + j) % 32 < G.

@@ -38,15 +38,50 @@ __global__ void __launch_bounds__(SC_THREADS)
 // producer starts streaming BEFORE griddepcontrol.wait — `in` is not written by
 // the preceding reduce — so under PDL the first chunks overlap the reduce's
 // tail; no store happens before the wait (out may alias in).
+// ctr != NULL: chunks are dealt from a queue (the producer claims the next chunk
+// with an atomic, one ahead) instead of grid-strided, so SMs that stream faster
+// take more chunks and the grid finishes together; every output element is the
+// same quotient whoever computes it, so this changes no bits.  The last producer
+// to run dry resets the queue for the next call.
 __global__ void __launch_bounds__(BK_THREADS, 1)
     scale_bulk_kernel(float* out, const float* in, int64_t len, const double* __restrict__ S_parts,
-                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
+                      int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch,
+                      unsigned* ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[SB_STAGES], empty[SB_STAGES];
+  __shared__ int64_t stage_chunk[SB_STAGES];
   __shared__ float s_sh;
   auto r = bulk_ring_init<SB_STAGES, SB_CHUNK>(ring, full, empty);
+  constexpr int64_t CF = SB_CHUNK / 4;
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) bulk_produce<false>(r, in, len, 0);
+    if (threadIdx.x == 0) {
+      if (!ctr) {
+        bulk_produce<false>(r, in, len, 0);
+      } else {
+        int64_t head, nchunks;
+        bulk_split<CF>(in, len, &head, &nchunks);
+        const float* body = in + head;
+        int64_t next = (int64_t)atomicAdd(ctr, 1u);
+        for (;;) {
+          const int64_t c = next;
+          if (c >= nchunks) break;
+          next = (int64_t)atomicAdd(ctr, 1u);
+          if (r.issued >= SB_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+          stage_chunk[r.stage] = c;
+          mbar_arrive_expect_tx(&r.full[r.stage], SB_CHUNK);
+          bulk_g2s(r.buf + (size_t)r.stage * SB_CHUNK, body + c * CF, SB_CHUNK, &r.full[r.stage]);
+          ++r.issued;
+          r.advance();
+        }
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every producer has claimed its last chunk
+          ctr[0] = 0u;
+          ctr[1] = 0u;
+        }
+        if (r.issued >= SB_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+        stage_chunk[r.stage] = -1;  // end marker: completes with no bytes
+        mbar_arrive(&r.full[r.stage]);
+      }
+    }
     return;
   }
   const int ct = threadIdx.x - 32;
@@ -61,7 +96,34 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
-  bulk_scale_consume(r, out, in, len, make_divisor(s_sh), ct);
+  const Divisor dv = make_divisor(s_sh);
+  if (!ctr) {
+    bulk_scale_consume(r, out, in, len, dv, ct);
+    return;
+  }
+  int64_t head, nchunks;
+  bulk_split<CF>(in, len, &head, &nchunks);
+  float* ob = out + head;
+  for (;;) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const int64_t c = *(volatile int64_t*)&stage_chunk[r.stage];
+    if (c < 0) break;
+    const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * SB_CHUNK);
+    float* oc = ob + c * CF;
+#pragma unroll
+    for (int k = 0; k < SB_CHUNK / 32 / BK_CONSUMERS; ++k) {
+      const int i = k * BK_CONSUMERS + ct;
+      const float4 a = q[2 * i], b = q[2 * i + 1];
+      st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
+    }
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
+  for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
+       i += (int64_t)gridDim.x * BK_CONSUMERS)
+    out[i] = div_rn(in[i], dv);
+  if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
 }
 
 __global__ void __launch_bounds__(256)
@@ -110,7 +172,7 @@ __global__ void __launch_bounds__(SMALL_THREADS)
 
 cudaError_t launch_scale(float* out, const float* in, int64_t len, const double* S_parts,
                          int nparts, float* sum_out, double* sum_out_f64, const DeviceInfo& d,
-                         bool pdl, cudaStream_t st, unsigned long long epoch) {
+                         bool pdl, cudaStream_t st, unsigned long long epoch, unsigned* ctr) {
   const int64_t per_chunk = (int64_t)SC_THREADS * SC_UNROLL * 8;
   int64_t g = (len + per_chunk - 1) / per_chunk;
   const int64_t gmax = (int64_t)d.sms * SC_CTAS_PER_SM;
@@ -126,8 +188,13 @@ cudaError_t launch_scale(float* out, const float* in, int64_t len, const double*
       if (e != cudaSuccess) return e;
       configured[d.device] = 1;
     }
+    static const bool queue = [] {
+      const char* e = getenv("NORM_SCALE_QUEUE");
+      return !(e && !strcmp(e, "0"));
+    }();
     return launch_maybe_pdl_smem(scale_bulk_kernel, d.sms, BK_THREADS, SB_SMEM, pdl, st, out, in,
-                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch);
+                                 len, S_parts, nparts, sum_out, sum_out_f64, epoch,
+                                 queue ? ctr : (unsigned*)nullptr);
   }
   if (vec && alias)
     return launch_maybe_pdl(scale_kernel<true, true>, (int)g, SC_THREADS, pdl, st, out, in, len,
