@@ -327,7 +327,7 @@ norm_status_t norm_launch_sharded_peer(norm_peer_t* peer, float* out_local, cons
                                        const norm_opts_t* o);
 
 /* --------------------------------------------------------------- caches */
-/* Frees libnorm's internal per-(device, stream) caches: the ~33 KB workspaces and
+/* Frees libnorm's internal per-(device, stream) caches: the ~161 KB workspaces and
  * the norm_launch_host staging buffers (resident covered prefix, 3 x 128 MiB ring).
  * Synchronises every device that owns a cache entry.  Later calls re-create them.
  * Note for CUDA-graph capture: the internal workspace of a (device, stream) is
