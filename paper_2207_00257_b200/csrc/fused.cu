@@ -44,29 +44,27 @@ template <bool VEC>
 __global__ void __launch_bounds__(BK_THREADS, 1)
     fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
                  unsigned* bar, float* sum_out, double* sum_out_f64, int hints, PeerPost post,
-                 const double* mailbox) {
+                 const double* mailbox, unsigned* task_ctr, double* task_sums, int64_t dyn, int tc) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
+  __shared__ DynSmem dsm;
   __shared__ double red[BK_THREADS / 32];
   __shared__ double S_sh;
+  if (threadIdx.x < 2) dsm.slot_cnt[threadIdx.x] = 0u;
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
-  double acc = 0.0;
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      if (hints >= 2) bulk_produce<true>(r, in + L, n - L, policy_evict_first());
-      else bulk_produce<false>(r, in + L, n - L, 0);
-      if (hints >= 1) bulk_produce<true>(r, in, L, policy_evict_last());
-      else bulk_produce<false>(r, in, L, 0);
-    }
-  } else {
-    bulk_consume(r, in + L, n - L, acc, threadIdx.x - 32);
-    bulk_consume(r, in, L, acc, threadIdx.x - 32);
-  }
+  // phase 1: the tail, then the covered prefix (read last), with a dynamic,
+  // deterministic end (dyn_stream_sum)
+  const DynSeg seg[2] = {{in + L, n - L, policy_evict_first(), hints >= 2 ? 1 : 0},
+                         {in, L, policy_evict_last(), hints >= 1 ? 1 : 0}};
+  int64_t ntasks;
+  const double acc = dyn_stream_sum<2>(r, seg, dyn, tc, task_ctr, task_sums, dsm, &ntasks);
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
   grid_barrier(bar);  // all of `in` has been read: `out` (possibly == in) may be written
+  if (blockIdx.x == 0 && threadIdx.x == 0) *task_ctr = 0u;  // every CTA is done claiming
   double v = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
+  for (int64_t t = threadIdx.x; t < ntasks; t += BK_THREADS) v += __ldcg(task_sums + t);
   double S = block_sum(v, red);  // identical bits in every CTA
   if (post.mail) {
     if (threadIdx.x == 0) {
@@ -117,8 +115,13 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
   double* partials = ws.partials;
   unsigned* bar = ws.bar;
   int hints = fused_hints(cov, d);
+  unsigned* task_ctr = ws.task_ctr;
+  double* task_sums = ws.task_sums;
+  int tc = 0;
+  int64_t dyn = dyn_chunks(n, &tc);
+  if (tc < kDynMinTC) tc = kDynMinTC;
   void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64, &hints,
-                  &post, (void*)&mailbox};
+                  &post, (void*)&mailbox, &task_ctr, &task_sums, &dyn, &tc};
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BK_THREADS), args, BK_SMEM, st);
 }
 

@@ -99,6 +99,10 @@ cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float
 
 // One cooperative persistent kernel: reduce (covered prefix last, L2 evict_last),
 // grid barrier, scale from L2.  Requires COV_PREFIX.
+// Chunks of an n-element stream that the bulk reduce / fused kernel hand out
+// dynamically (NORM_DYN_PCT / NORM_DYN_TC; reduce.cu), and the task size.
+int64_t dyn_chunks(int64_t n, int* tc);
+
 // post.mail set: multi-GPU, the rank partial is published into every rank's
 // mailbox after the grid barrier and `mailbox` (this rank's) is waited on.
 cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const Workspace& ws,

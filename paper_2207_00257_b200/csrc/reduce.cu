@@ -82,21 +82,10 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
 }
 
-// Pass 1, TMA-bulk with a dynamically scheduled, still deterministic tail.
-// Measured (scripts/reduce_timeline.cu): with every chunk dealt statically the
-// per-SM streaming rates differ by ~1-2 % at random, so the last CTA finishes
-// ~20-40 us after the median at n = 2^32 (~6 us at 2^29) while the others idle.
-// Here the first nchunks - dyn chunks are dealt grid-strided as in
-// reduce_bulk_kernel (one partial per CTA), and the last `dyn` chunks form tasks
-// of `tc` consecutive chunks that CTAs claim with an atomic counter as they run
-// dry.  Determinism does not depend on who runs a task: a task's sum is formed
-// in a fixed order (each consumer thread over its groups of the task's chunks in
-// chunk order, warp butterfly, then the 8 warp sums in warp order by whichever
-// warp finishes the task last) and stored in task_sums[t]; the last CTA adds the
-// per-CTA partials and then the task sums in index order.  tc >= BK_STAGES, so a
-// warp can be at most one task ahead of another (double-buffered task slots).
-constexpr int kDynMinTC = BK_STAGES;
-
+// Pass 1, TMA-bulk with a dynamically scheduled, still deterministic tail
+// (dyn_stream_sum, stream_common.cuh): per-CTA partials for the grid-strided
+// chunks, task sums for the last `dyn` chunks; the last CTA adds the partials,
+// then the task sums, in index order.
 __global__ void __launch_bounds__(BK_THREADS, 1)
     reduce_dyn_kernel(const float* __restrict__ in, int64_t n, double* __restrict__ partials,
                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
@@ -105,102 +94,14 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   if (early_trigger) pdl_launch_dependents();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
-  __shared__ int64_t stage_chunk[BK_STAGES];  // dynamic part: chunk index in flight, -1 = no more
+  __shared__ DynSmem dsm;
   __shared__ double red[BK_THREADS / 32];
-  __shared__ double slot[2][BK_CONSUMERS / 32];
-  __shared__ unsigned slot_cnt[2];
   __shared__ unsigned is_last;
-  if (threadIdx.x < 2) slot_cnt[threadIdx.x] = 0u;
+  if (threadIdx.x < 2) dsm.slot_cnt[threadIdx.x] = 0u;
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
-  constexpr int64_t CF = BulkRing<BK_STAGES, BK_CHUNK>::CF;
-  int64_t head, nchunks;
-  bulk_split<CF>(in, n, &head, &nchunks);
-  const float* body = in + head;
-  if (dyn > nchunks) dyn = nchunks;
-  const int64_t ns = nchunks - dyn;                // static chunks [0, ns)
-  const int64_t ntasks = (dyn + tc - 1) / tc;      // dynamic chunks [ns, nchunks)
-  double acc = 0.0;
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      BulkCursor cur{body, (int64_t)blockIdx.x, ns};
-      bulk_issue<false>(r, cur, INT64_MAX, 0);
-      // claim one task ahead, so the atomic's round trip overlaps a task's loads
-      int64_t next = ntasks > 0 ? (int64_t)atomicAdd(task_ctr, 1u) : ntasks;
-      for (;;) {
-        const int64_t t = next;
-        if (t < ntasks) next = (int64_t)atomicAdd(task_ctr, 1u);
-        const int64_t c0 = ns + t * tc, c1 = t < ntasks ? (c0 + tc < nchunks ? c0 + tc : nchunks) : c0;
-        for (int64_t c = c0; c < c1; ++c) {
-          if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
-          stage_chunk[r.stage] = c;
-          mbar_arrive_expect_tx(&r.full[r.stage], BK_CHUNK);
-          bulk_g2s(r.buf + (size_t)r.stage * BK_CHUNK, body + c * CF, BK_CHUNK, &r.full[r.stage]);
-          ++r.issued;
-          r.advance();
-        }
-        if (t >= ntasks) break;
-      }
-      // end marker: a stage whose full barrier completes with no bytes
-      if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
-      stage_chunk[r.stage] = -1;
-      mbar_arrive(&r.full[r.stage]);
-    }
-  } else {
-    const int ct = threadIdx.x - 32, w = ct >> 5, lane = ct & 31;
-    for (int64_t c = blockIdx.x; c < ns; c += gridDim.x) {  // static part, as bulk_consume
-      mbar_wait(&r.full[r.stage], r.phase);
-      const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
-#pragma unroll
-      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
-        const int i = k * BK_CONSUMERS + ct;
-        const float4 a = q[2 * i], b = q[2 * i + 1];
-        acc += sum8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}});
-      }
-      stage_release(&r.empty[r.stage]);
-      r.advance();
-    }
-    double tacc = 0.0;
-    unsigned done = 0;  // tasks finished by this warp (same sequence in every warp)
-    for (;;) {
-      mbar_wait(&r.full[r.stage], r.phase);
-      const int64_t c = *(volatile int64_t*)&stage_chunk[r.stage];
-      if (c < 0) break;
-      const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
-#pragma unroll
-      for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
-        const int i = k * BK_CONSUMERS + ct;
-        const float4 a = q[2 * i], b = q[2 * i + 1];
-        tacc += sum8(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}});
-      }
-      stage_release(&r.empty[r.stage]);
-      r.advance();
-      const int64_t d = c - ns;
-      if ((d + 1) % tc == 0 || c + 1 == nchunks) {  // last chunk of task d / tc
-        const double v = warp_sum(tacc);
-        tacc = 0.0;
-        const unsigned p = done++ & 1u;
-        if (lane == 0) {
-          slot[p][w] = v;
-          __threadfence_block();
-          if (atomicAdd(&slot_cnt[p], 1u) == BK_CONSUMERS / 32 - 1) {
-            __threadfence_block();
-            double t = 0.0;
-#pragma unroll
-            for (int k = 0; k < BK_CONSUMERS / 32; ++k) t += *(volatile double*)&slot[p][k];
-            task_sums[d / tc] = t;
-            __threadfence();  // before this CTA's ticket: the last CTA reads task_sums
-            slot_cnt[p] = 0u;
-          }
-        }
-      }
-    }
-    // remainder (< one chunk) and head: plain loads into the static partial
-    const int64_t rbeg = head + nchunks * CF;
-    for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < n;
-         i += (int64_t)gridDim.x * BK_CONSUMERS)
-      acc += (double)in[i];
-    if (blockIdx.x == 0 && ct < head) acc += (double)in[ct];
-  }
+  const DynSeg seg[1] = {{in, n, 0, 0}};
+  int64_t ntasks;
+  const double acc = dyn_stream_sum<1>(r, seg, dyn, tc, task_ctr, task_sums, dsm, &ntasks);
   if (!early_trigger) pdl_launch_dependents();
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
@@ -249,7 +150,7 @@ int pdl_mode() {
 // (NORM_DYN_TC, default kDynTC, >= BK_STAGES), capped at kMaxTasks tasks.
 constexpr int kDynPct = 3, kDynTC = 8;  // profiles/r05/dyn_sweep2.txt
 
-static int64_t dyn_chunks(int64_t n, int* tc_out) {
+int64_t dyn_chunks(int64_t n, int* tc_out) {
   static const int pct = [] {
     const char* e = getenv("NORM_DYN_PCT");
     return e ? atoi(e) : kDynPct;

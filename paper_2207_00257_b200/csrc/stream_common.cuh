@@ -275,6 +275,186 @@ __device__ __forceinline__ BulkRing<STAGES, CHUNK> bulk_ring_init(unsigned char*
   return BulkRing<STAGES, CHUNK>{buf, full, empty, 0, 0u, 0};
 }
 
+// ---- dynamically scheduled, deterministic streaming sum ----------------------
+// The hoisted `sum` over up to NSEG segments (streamed in segment order, each
+// with its own L2 policy) through the BK ring.  Chunk u of the concatenated
+// chunk space: the first `ns` are dealt grid-strided (they feed this CTA's
+// partial `acc`), the last `dyn` form tasks of `tc` consecutive chunks that CTAs
+// claim from *task_ctr as they run dry (claimed one ahead, so the atomic's round
+// trip overlaps the loads).  A task's sum does not depend on which CTA runs it:
+// each consumer thread adds its 8-float groups of the task's chunks in chunk
+// order, a warp butterfly combines the lanes, and whichever warp finishes the
+// task last adds the 8 warp sums in warp order into task_sums[t].  tc >=
+// BK_STAGES bounds how far warps drift apart (at most one task), so two task
+// slots suffice.  Why: per-SM streaming rates differ by 1-2 % at random, and
+// with every chunk dealt statically the last CTA finished ~20-40 us after the
+// median at n = 2^32 (scripts/reduce_timeline.cu).  The caller combines
+// per-CTA partials and task sums in index order, and resets *task_ctr once
+// every CTA is done claiming.
+constexpr int kDynMinTC = BK_STAGES;
+
+struct DynSeg {
+  const float* p;
+  int64_t len;
+  uint64_t pol;
+  int hint;  // 1: cp.async.bulk with the L2 policy `pol`
+};
+
+struct DynSmem {  // shared-memory state of dyn_stream_sum
+  int64_t stage_chunk[BK_STAGES];
+  double slot[2][BK_CONSUMERS / 32];
+  unsigned slot_cnt[2];
+};
+
+template <int NSEG>
+struct DynGeo {
+  const float* body[NSEG];
+  int64_t head[NSEG], nch[NSEG];
+  int64_t total;
+  __device__ __forceinline__ DynGeo(const DynSeg* seg) : total(0) {
+    constexpr int64_t CF = BK_CHUNK / 4;
+#pragma unroll
+    for (int i = 0; i < NSEG; ++i) {
+      if (seg[i].len > 0) {
+        bulk_split<CF>(seg[i].p, seg[i].len, &head[i], &nch[i]);
+      } else {
+        head[i] = 0;
+        nch[i] = 0;
+      }
+      body[i] = seg[i].p + head[i];
+      total += nch[i];
+    }
+  }
+  __device__ __forceinline__ const float* chunk(int64_t u, int* si) const {
+    constexpr int64_t CF = BK_CHUNK / 4;
+#pragma unroll
+    for (int i = 0; i < NSEG - 1; ++i) {
+      if (u < nch[i]) {
+        *si = i;
+        return body[i] + u * CF;
+      }
+      u -= nch[i];
+    }
+    *si = NSEG - 1;
+    return body[NSEG - 1] + u * CF;
+  }
+};
+
+template <int NSEG>
+__device__ __forceinline__ void dyn_issue(BulkRing<BK_STAGES, BK_CHUNK>& r, const DynGeo<NSEG>& g,
+                                          const DynSeg* seg, int64_t u, DynSmem& sm, bool tag) {
+  int si;
+  const float* src = g.chunk(u, &si);
+  if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+  if (tag) sm.stage_chunk[r.stage] = u;
+  mbar_arrive_expect_tx(&r.full[r.stage], BK_CHUNK);
+  void* dst = r.buf + (size_t)r.stage * BK_CHUNK;
+  uint64_t pol = seg[0].pol;  // select without dynamic indexing (keeps seg in registers)
+  int hint = seg[0].hint;
+#pragma unroll
+  for (int i = 1; i < NSEG; ++i)
+    if (si == i) {
+      pol = seg[i].pol;
+      hint = seg[i].hint;
+    }
+  if (hint) bulk_g2s_hint(dst, src, BK_CHUNK, &r.full[r.stage], pol);
+  else bulk_g2s(dst, src, BK_CHUNK, &r.full[r.stage]);
+  ++r.issued;
+  r.advance();
+}
+
+__device__ __forceinline__ double dyn_chunk_sum(const BulkRing<BK_STAGES, BK_CHUNK>& r, int ct) {
+  const float4* q = reinterpret_cast<const float4*>(r.buf + (size_t)r.stage * BK_CHUNK);
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < BK_CHUNK / 32 / BK_CONSUMERS; ++k) {
+    const int i = k * BK_CONSUMERS + ct;
+    const float4 x = q[2 * i], y = q[2 * i + 1];
+    a += sum8(f8{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}});
+  }
+  return a;
+}
+
+// Called by every thread of a BK_THREADS CTA (warp 0 lane 0 produces, warps 1..8
+// consume); returns this thread's share of the CTA's static partial.  `sm` must
+// have slot_cnt zeroed before the ring's init barrier.
+template <int NSEG>
+__device__ __forceinline__ double dyn_stream_sum(BulkRing<BK_STAGES, BK_CHUNK>& r, const DynSeg* seg,
+                                                 int64_t dyn, int tc, unsigned* task_ctr,
+                                                 double* task_sums, DynSmem& sm, int64_t* ntasks_out) {
+  const DynGeo<NSEG> g(seg);
+  if (dyn > g.total) dyn = g.total;
+  const int64_t ns = g.total - dyn;
+  const int64_t ntasks = (dyn + tc - 1) / tc;
+  *ntasks_out = ntasks;
+  double acc = 0.0;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      for (int64_t u = blockIdx.x; u < ns; u += gridDim.x) dyn_issue<NSEG>(r, g, seg, u, sm, false);
+      int64_t next = ntasks > 0 ? (int64_t)atomicAdd(task_ctr, 1u) : ntasks;
+      while (next < ntasks) {
+        const int64_t t = next;
+        next = (int64_t)atomicAdd(task_ctr, 1u);
+        const int64_t u0 = ns + t * tc, u1 = u0 + tc < g.total ? u0 + tc : g.total;
+        for (int64_t u = u0; u < u1; ++u) dyn_issue<NSEG>(r, g, seg, u, sm, true);
+      }
+      if (r.issued >= BK_STAGES) stage_acquire(&r.empty[r.stage], r.phase ^ 1);
+      sm.stage_chunk[r.stage] = -1;  // end marker: completes with no bytes
+      mbar_arrive(&r.full[r.stage]);
+    }
+    return 0.0;
+  }
+  const int ct = threadIdx.x - 32, w = ct >> 5, lane = ct & 31;
+  for (int64_t u = blockIdx.x; u < ns; u += gridDim.x) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    acc += dyn_chunk_sum(r, ct);
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+  }
+  double tacc = 0.0;
+  unsigned done = 0;  // tasks this warp has finished (the same sequence in every warp)
+  for (;;) {
+    mbar_wait(&r.full[r.stage], r.phase);
+    const int64_t u = *(volatile int64_t*)&sm.stage_chunk[r.stage];
+    if (u < 0) break;
+    tacc += dyn_chunk_sum(r, ct);
+    stage_release(&r.empty[r.stage]);
+    r.advance();
+    const int64_t d = u - ns;
+    if ((d + 1) % tc == 0 || u + 1 == g.total) {  // last chunk of task d / tc
+      const double v = warp_sum(tacc);
+      tacc = 0.0;
+      const unsigned p = done++ & 1u;
+      if (lane == 0) {
+        sm.slot[p][w] = v;
+        __threadfence_block();
+        if (atomicAdd(&sm.slot_cnt[p], 1u) == BK_CONSUMERS / 32 - 1) {
+          __threadfence_block();
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k < BK_CONSUMERS / 32; ++k) t += *(volatile double*)&sm.slot[p][k];
+          task_sums[d / tc] = t;
+          __threadfence();  // before this CTA's ticket / grid barrier
+          sm.slot_cnt[p] = 0u;
+        }
+      }
+    }
+  }
+  // each segment's remainder (< one chunk) and head: plain loads, static
+  constexpr int64_t CF = BK_CHUNK / 4;
+#pragma unroll
+  for (int i = 0; i < NSEG; ++i) {
+    const float* p = seg[i].p;
+    const int64_t len = seg[i].len;
+    if (len <= 0) continue;
+    for (int64_t e = g.head[i] + g.nch[i] * CF + (int64_t)blockIdx.x * BK_CONSUMERS + ct; e < len;
+         e += (int64_t)gridDim.x * BK_CONSUMERS)
+      acc += (double)p[e];
+    if (blockIdx.x == 0 && ct < g.head[i]) acc += (double)p[ct];
+  }
+  return acc;
+}
+
 // ---- rank partials (multi-GPU) ---------------------------------------------
 // Fused exchange: the rank's partial goes straight from the reduce's last CTA into
 // slot [epoch & 1][rank] of every rank's mailbox (peer stores through NVLink),
