@@ -11,7 +11,8 @@ import gen, paper_2207_00257_b200 as L
 torch.cuda.set_device(0)
 for n, path in [(1000, "small"), (5000, "two_pass"), (2**20 + 7, "two_pass"), (2**20 + 7, "fused"),
                 (3 * 2**20 + 5, "two_pass"), (2**22 + 9, "two_pass"), (700, "two_pass"),
-                (2**24 + 3, "two_pass"), (2**25, "fused")]:  # many chunks per CTA: ring stages reused
+                (2**24 + 3, "two_pass"), (2**25, "fused"),  # many chunks per CTA: ring stages reused
+                (2**26 + 5, "two_pass"), (2**26 + 5, "fused")]:  # dynamic reduce tail: 16 tasks
     for mode in ("literal", "dense"):
         x = torch.from_numpy(gen.make_host(n, seed=1, dist=0)).cuda()
         y = torch.zeros_like(x)
