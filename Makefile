@@ -47,6 +47,12 @@ $(PKG)/faults/libnorm_fault%.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DNORM_FAULT=$* -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> /dev/null
 
+# Timeline probe build (scripts/fused_timeline.py only; never loaded by the product)
+$(PKG)/faults/libnorm_timeline.so: $(CSRC) $(CHDR)
+	@mkdir -p $(PKG)/faults
+	$(NVCC) $(NVFLAGS) -DNORM_TIMELINE -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> /dev/null
+
 clean:
 	rm -f oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
 	rm -rf $(PKG)/faults

@@ -9,20 +9,40 @@
 
 namespace lnorm {
 
+
+#ifdef NORM_TIMELINE  // probe builds only (scripts/fused_timeline.py): per-CTA %globaltimer stamps
+__device__ unsigned long long g_fused_ts[4096 * 5];
+__device__ __forceinline__ unsigned long long stamp_ns() {  // ordered with memory ops
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+#define FUSED_STAMP(k)                                                         \
+  if (threadIdx.x == 32) g_fused_ts[blockIdx.x * 5 + (k)] = stamp_ns();
+#else
+#define FUSED_STAMP(k)
+#endif
+
 // ---------------------------------------------------------------- fused
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+// Grid-wide barrier of a cooperative launch (one per kernel): bar = {count,
+// generation}.  Each CTA's thread 0 read the generation at kernel start (`gen`;
+// it only changes at this barrier), arrives with an acq_rel add (its CTA's prior
+// writes released; the last arriver acquires everyone's); the last arriver
+// resets the count and publishes gen + 1 with a release store; the others spin
+// on an acquire load of the generation.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_u32(bar + 1);
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    if (atom_add_acq_rel_u32(bar, 1u) == gridDim.x - 1) {
+      st_relaxed_u32(bar, 0u);
+      st_release_u32(bar + 1, gen + 1u);
     } else {
-      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(40);
+      while (ld_acquire_u32(bar + 1) == gen) {
+      }
     }
-    __threadfence();
+#ifdef NORM_TIMELINE
+    g_fused_ts[blockIdx.x * 5 + 2] = stamp_ns();  // thread 0 out of the spin
+#endif
   }
   __syncthreads();
 }
@@ -50,6 +70,8 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   __shared__ DynSmem dsm;
   __shared__ double red[BK_THREADS / 32];
   __shared__ double S_sh;
+  FUSED_STAMP(0)
+  const unsigned gen = threadIdx.x == 0 ? ld_acquire_u32(bar + 1) : 0u;  // grid_barrier's generation
   if (threadIdx.x < 2) dsm.slot_cnt[threadIdx.x] = 0u;
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   // phase 1: the tail, then the covered prefix (read last), with a dynamic,
@@ -58,9 +80,10 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
                          {in, L, policy_evict_last(), hints >= 1 ? 1 : 0}};
   int64_t ntasks;
   const double acc = dyn_stream_sum<2>(r, seg, dyn, tc, task_ctr, task_sums, dsm, &ntasks);
+  FUSED_STAMP(1)
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
-  grid_barrier(bar);  // all of `in` has been read: `out` (possibly == in) may be written
+  grid_barrier(bar, gen);  // all of `in` has been read: `out` (possibly == in) may be written
   if (blockIdx.x == 0 && threadIdx.x == 0) *task_ctr = 0u;  // every CTA is done claiming
   double v = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
@@ -81,8 +104,17 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     if (sum_out) *sum_out = s;
     if (sum_out_f64) *sum_out_f64 = S;
   }
+  FUSED_STAMP(3)
   scale_segment<BK_THREADS, FU_SCALE_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
+  FUSED_STAMP(4)
 }
+
+#ifdef NORM_TIMELINE
+extern "C" __attribute__((visibility("default"))) int norm_debug_fused_timeline(unsigned long long* host,
+                                                                                 int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_fused_ts, (size_t)n * sizeof(unsigned long long));
+}
+#endif
 
 // L2 hint policy (kernel comment): 2 while the covered prefix is <= L2/3, else 1.
 // NORM_FUSED_HINTS=0|1|2 overrides (A/B experiments), read once.
@@ -118,7 +150,7 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
   unsigned* task_ctr = ws.task_ctr;
   double* task_sums = ws.task_sums;
   int tc = 0;
-  int64_t dyn = dyn_chunks(n, &tc);
+  int64_t dyn = dyn_chunks(n, grid, &tc);
   if (tc < kDynMinTC) tc = kDynMinTC;
   void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64, &hints,
                   &post, (void*)&mailbox, &task_ctr, &task_sums, &dyn, &tc};

@@ -101,7 +101,7 @@ cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float
 // grid barrier, scale from L2.  Requires COV_PREFIX.
 // Chunks of an n-element stream that the bulk reduce / fused kernel hand out
 // dynamically (NORM_DYN_PCT / NORM_DYN_TC; reduce.cu), and the task size.
-int64_t dyn_chunks(int64_t n, int* tc);
+int64_t dyn_chunks(int64_t n, int grid, int* tc);
 
 // post.mail set: multi-GPU, the rank partial is published into every rank's
 // mailbox after the grid barrier and `mailbox` (this rank's) is waited on.

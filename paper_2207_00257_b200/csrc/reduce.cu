@@ -145,25 +145,36 @@ int pdl_mode() {
   return mode;
 }
 
-// Dynamic tail of the bulk reduce: `frac` of the chunks (NORM_DYN_PCT percent,
-// default kDynPct; 0 = fully static reduce_bulk_kernel) in tasks of tc chunks
-// (NORM_DYN_TC, default kDynTC, >= BK_STAGES), capped at kMaxTasks tasks.
+// Dynamic tail of the bulk reduce / fused phase 1: the last pct % of the chunks
+// (NORM_DYN_PCT, default kDynPct; 0 = fully static reduce_bulk_kernel) but at
+// least kDynMinTasksPerCTA tasks per CTA, so smaller inputs still get a fine
+// enough tail (2^28: 3 % would be fewer tasks than CTAs), in tasks of tc chunks
+// (NORM_DYN_TC, default kDynTC; kDynMinTC at those sizes), at most half the
+// chunks and kMaxTasks tasks.
 constexpr int kDynPct = 3, kDynTC = 8;  // profiles/r05/dyn_sweep2.txt
+constexpr int kDynMinTasksPerCTA = 4;
 
-int64_t dyn_chunks(int64_t n, int* tc_out) {
+int64_t dyn_chunks(int64_t n, int grid, int* tc_out) {
   static const int pct = [] {
     const char* e = getenv("NORM_DYN_PCT");
     return e ? atoi(e) : kDynPct;
   }();
-  static const int tc = [] {
+  static const int tc_env = [] {
     const char* e = getenv("NORM_DYN_TC");
     const int v = e ? atoi(e) : kDynTC;
     return v < kDynMinTC ? kDynMinTC : v;
   }();
-  *tc_out = tc;
   const int64_t nchunks = n / (BK_CHUNK / 4);
+  int tc = tc_env;
   int64_t dyn = nchunks * pct / 100;
+  const int64_t floor_tasks = (int64_t)kDynMinTasksPerCTA * grid;
+  if (dyn < floor_tasks * tc) {  // too few tasks: smallest tasks, and at least floor_tasks of them
+    tc = kDynMinTC;
+    if (dyn < floor_tasks * tc) dyn = floor_tasks * tc;
+  }
+  if (dyn > nchunks / 2) dyn = nchunks / 2;
   if (dyn > (int64_t)kMaxTasks * tc) dyn = (int64_t)kMaxTasks * tc;
+  *tc_out = tc;
   return pct > 0 ? dyn : 0;
 }
 
@@ -182,7 +193,7 @@ cudaError_t launch_reduce(const float* in, int64_t n, const Workspace& ws, doubl
       configured[d.device] = 1;
     }
     int tc = 0;
-    const int64_t dyn = dyn_chunks(n, &tc);
+    const int64_t dyn = dyn_chunks(n, d.sms, &tc);
     if (dyn > 0) {
       static int configured_dyn[64] = {0};
       if (d.device < 64 && !configured_dyn[d.device]) {
