@@ -142,6 +142,7 @@ Workspace workspace_carve(void* base) {
   w.bar = w.ticket + 1;
   w.task_ctr = w.ticket + 4;
   w.scale_ctr = w.ticket + 6;
+  w.row_ctr = w.ticket + 8;
   p += 256;
   w.task_sums = reinterpret_cast<double*>(p);
   return w;
@@ -625,8 +626,10 @@ NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int6
   if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
   if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
   if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  Workspace ws;
+  if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_rows(out, in, rows, cols, ld_out, ld_in, rc, o->sum_out, o->sum_out_f64, d,
-                              static_cast<cudaStream_t>(o->stream));
+                              static_cast<cudaStream_t>(o->stream), ws.row_ctr);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows_kernel launch");
 }
 

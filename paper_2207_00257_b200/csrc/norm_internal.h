@@ -34,6 +34,7 @@ struct Workspace {
   unsigned* bar;       // [2] grid barrier {count, generation} of the fused kernel
   unsigned* task_ctr;  // [1] next task of the bulk reduce's dynamic tail
   unsigned* scale_ctr; // [2] {next chunk, producers done} of the bulk scale's chunk queue
+  unsigned* row_ctr;   // [2] {next row, CTAs done} of the register rows kernel's row queue
   double* task_sums;   // [kMaxTasks] per-task sums of the dynamic tail
 };
 size_t workspace_bytes();
@@ -111,9 +112,12 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
                          const double* mailbox = nullptr);
 
 // Batched rows: one CTA per row (grid-strided), row held in registers when it fits.
+// row_ctr (Workspace::row_ctr, zeroed; left zeroed) or NULL: rows dealt from a
+// queue or grid-strided.
 cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                         int64_t ld_in, const Coverage& row_cov, float* sum_out,
-                        double* sum_out_f64, const DeviceInfo& d, cudaStream_t st);
+                        double* sum_out_f64, const DeviceInfo& d, cudaStream_t st,
+                        unsigned* row_ctr = nullptr);
 
 // Fig. 1 before LICM (unhoisted.cu): the printed launch <<<(n+31)/32, 32>>> with
 // `sum` per thread (NORM_FORM_PER_THREAD) or per block (NORM_FORM_PER_BLOCK).

@@ -60,26 +60,62 @@ __device__ __forceinline__ void row_finish(float* dst, int nvr, const f8* v, int
 
 __host__ __device__ constexpr int row_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : ROW_CTAS_PER_SM; }
 
+// ctr != NULL: rows come from a queue instead of r, r + grid, ...: thread 0
+// claims the row after next with an atomic while the current row is finished (the
+// claim's round trip overlaps the row) and publishes it through shared memory
+// across the row's barrier; CTAs on faster SMs take more rows, so the grid ends
+// together.  Each row's result is independent of which CTA computes it.  The
+// last CTA to run dry resets the queue.
 template <bool ALIAS, int MAXV>
 __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
     rows_vec_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
-                    int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64) {
+                    int64_t ld_in, int64_t L, int64_t G, float* sum_out, double* sum_out_f64,
+                    unsigned* ctr) {
   __shared__ double red[2][ROW_THREADS / 32];  // alternated by row: one barrier per row
+  __shared__ int64_t claim[2];
   const int nvr = (int)(cols >> 3);
   const int64_t step = gridDim.x;
   f8 a[MAXV], b[MAXV];
-  int64_t r = blockIdx.x;
+  int64_t r, rn;
+  if (ctr) {
+    if (threadIdx.x == 0) {
+      claim[0] = (int64_t)atomicAdd(ctr, 1u);
+      claim[1] = claim[0] < rows ? (int64_t)atomicAdd(ctr, 1u) : rows;
+    }
+    __syncthreads();
+    r = claim[0];
+    rn = claim[1];
+  } else {
+    r = blockIdx.x;
+    rn = r + step;
+  }
+  // the row after rn: claimed by thread 0 before row_finish's barrier, read after it
+  auto next_after = [&](int64_t cur_next, int slot) -> int64_t {
+    if (!ctr) return cur_next + step;
+    return claim[slot];
+  };
+  auto claim_ahead = [&](int64_t cur_next, int slot) {
+    if (ctr && threadIdx.x == 0) claim[slot] = cur_next < rows ? (int64_t)atomicAdd(ctr, 1u) : rows;
+  };
   if (r < rows) row_load<ALIAS, MAXV>(in + r * ld_in, nvr, a);
   while (r < rows) {
-    int64_t rn = r + step;
     if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, b);
+    claim_ahead(rn, 0);
     row_finish<MAXV>(out + r * ld_out, nvr, a, r, L, G, red[0], sum_out, sum_out_f64);
+    int64_t rnn = next_after(rn, 0);
     r = rn;
+    rn = rnn;
     if (r >= rows) break;
-    rn = r + step;
     if (rn < rows) row_load<ALIAS, MAXV>(in + rn * ld_in, nvr, a);
+    claim_ahead(rn, 1);
     row_finish<MAXV>(out + r * ld_out, nvr, b, r, L, G, red[1], sum_out, sum_out_f64);
+    rnn = next_after(rn, 1);
     r = rn;
+    rn = rnn;
+  }
+  if (ctr && threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // all CTAs done claiming
+    ctr[0] = 0u;
+    ctr[1] = 0u;
   }
 }
 
@@ -189,7 +225,12 @@ __global__ void __launch_bounds__(ROW_THREADS)
 
 cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                         int64_t ld_in, const Coverage& rc, float* sum_out, double* sum_out_f64,
-                        const DeviceInfo& d, cudaStream_t st) {
+                        const DeviceInfo& d, cudaStream_t st, unsigned* row_ctr) {
+  static const bool queue = [] {
+    const char* e = getenv("NORM_ROWS_QUEUE");
+    return !(e && !strcmp(e, "0"));
+  }();
+  unsigned* rq = queue ? row_ctr : nullptr;
   const int maxv = cols <= ROW_THREADS * 8 ? 1 : (cols <= ROW_THREADS * 16 ? 2 : 4);
   int64_t g = (int64_t)d.sms * row_ctas_per_sm(maxv);  // persistent: one wave
   if (rows < g) g = rows;
@@ -228,7 +269,7 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
   }
 #define NORM_ROWS(A, M)                                                                           \
   rows_vec_kernel<A, M><<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, rc.G, \
-                                                       sum_out, sum_out_f64)
+                                                       sum_out, sum_out_f64, rq)
   if (!vec)
     rows_generic_kernel<<<(int)g, ROW_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, L, rc.G,
                                                         sum_out, sum_out_f64);
