@@ -652,8 +652,10 @@ NORM_API norm_status_t norm_softmax_rows(float* out, const float* in, int64_t ro
   if ((s = check_device(&d)) != NORM_OK) return s;
   if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
   if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  Workspace ws;
+  if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_softmax_rows(out, in, rows, cols, ld_out, ld_in, kind == NORM_LOG_SOFTMAX, d,
-                                      static_cast<cudaStream_t>(o->stream));
+                                      static_cast<cudaStream_t>(o->stream), ws.row_ctr);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "softmax kernel launch");
 }
 

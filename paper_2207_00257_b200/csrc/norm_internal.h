@@ -127,7 +127,7 @@ cudaError_t launch_unhoisted(float* out, const float* in, int64_t n, int index, 
 // NEXT-2 row ops (rowops.cu)
 cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
                                 int64_t ld_out, int64_t ld_in, bool log, const DeviceInfo& d,
-                                cudaStream_t st);
+                                cudaStream_t st, unsigned* row_ctr = nullptr);
 cudaError_t launch_nll_forward(float* loss, float* total_weight, const float* logp,
                                const int64_t* target, const float* weight, int64_t N, int64_t C,
                                int64_t ld, int reduction, int64_t ignore_index,

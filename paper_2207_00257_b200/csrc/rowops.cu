@@ -11,6 +11,8 @@
 // (zeros plus one value per row).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "device_common.cuh"
 #include "norm_internal.h"
@@ -107,27 +109,55 @@ __device__ __forceinline__ void sm_finish(float* dst, int nvr, f8* v, float* red
 
 __host__ __device__ constexpr int sm_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : 4; }
 
+// ctr != NULL: rows from a queue, as rows_vec_kernel (rows.cu): thread 0 claims
+// the row after next while the current row is finished and publishes it across
+// the row's barriers; the last CTA to run dry resets the queue.
 template <bool LOG, int MAXV>
 __global__ void __launch_bounds__(SM_THREADS, sm_ctas_per_sm(MAXV))
     softmax_vec_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
-                       int64_t ld_in) {
+                       int64_t ld_in, unsigned* ctr) {
   __shared__ float redf[SM_THREADS / 32];
   __shared__ double redd[SM_THREADS / 32];
+  __shared__ int64_t claim[2];
   const int nvr = (int)(cols >> 3);
   const int64_t step = gridDim.x;
   f8 a[MAXV], b[MAXV];
-  int64_t r = blockIdx.x;
+  int64_t r, rn;
+  if (ctr) {
+    if (threadIdx.x == 0) {
+      claim[0] = (int64_t)atomicAdd(ctr, 1u);
+      claim[1] = claim[0] < rows ? (int64_t)atomicAdd(ctr, 1u) : rows;
+    }
+    __syncthreads();
+    r = claim[0];
+    rn = claim[1];
+  } else {
+    r = blockIdx.x;
+    rn = r + step;
+  }
+  auto claim_ahead = [&](int64_t cur_next, int slot) {
+    if (ctr && threadIdx.x == 0) claim[slot] = cur_next < rows ? (int64_t)atomicAdd(ctr, 1u) : rows;
+  };
+  auto next_after = [&](int64_t cur_next, int slot) -> int64_t { return ctr ? claim[slot] : cur_next + step; };
   if (r < rows) sm_load<MAXV>(in + r * ld_in, nvr, a);
   while (r < rows) {
-    int64_t rn = r + step;
     if (rn < rows) sm_load<MAXV>(in + rn * ld_in, nvr, b);
+    claim_ahead(rn, 0);
     sm_finish<LOG, MAXV>(out + r * ld_out, nvr, a, redf, redd);
+    int64_t rnn = next_after(rn, 0);
     r = rn;
+    rn = rnn;
     if (r >= rows) break;
-    rn = r + step;
     if (rn < rows) sm_load<MAXV>(in + rn * ld_in, nvr, a);
+    claim_ahead(rn, 1);
     sm_finish<LOG, MAXV>(out + r * ld_out, nvr, b, redf, redd);
+    rnn = next_after(rn, 1);
     r = rn;
+    rn = rnn;
+  }
+  if (ctr && threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // all CTAs done claiming
+    ctr[0] = 0u;
+    ctr[1] = 0u;
   }
 }
 
@@ -252,7 +282,12 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
                                 int64_t ld_out, int64_t ld_in, bool log, const DeviceInfo& d,
-                                cudaStream_t st) {
+                                cudaStream_t st, unsigned* row_ctr) {
+  static const bool queue = [] {
+    const char* e = getenv("NORM_ROWS_QUEUE");
+    return !(e && !strcmp(e, "0"));
+  }();
+  unsigned* rq = queue ? row_ctr : nullptr;
   const bool aligned = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 31u) == 0 &&
                        (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
   const bool vec = aligned && out != in && cols <= (int64_t)SM_THREADS * 8 * 4;
@@ -260,7 +295,7 @@ cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64
   int64_t g = (int64_t)d.sms * (vec ? sm_ctas_per_sm(maxv) : 8);
   if (rows < g) g = rows;
 #define NORM_SM(LG, M) \
-  softmax_vec_kernel<LG, M><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in)
+  softmax_vec_kernel<LG, M><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in, rq)
   if (!vec) {
     if (log) softmax_generic_kernel<true><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in);
     else softmax_generic_kernel<false><<<(int)g, SM_THREADS, 0, st>>>(out, in, rows, cols, ld_out, ld_in);

@@ -130,12 +130,17 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
 constexpr int RB_MAX_STAGES = 16;
 constexpr size_t RB_SMEM_BUDGET = 200 * 1024;
 
+// ctr != NULL: the producer takes its grid-strided share of the first 97 % of the
+// rows, then claims rows of the rest from a queue (one ahead), tagging each stage
+// with its row (stage_row); after the last row it posts an end marker to each
+// consumer warp's next stage; the last producer to run dry resets the queue.
 __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
     rows_bulk_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                      int64_t ld_in, int64_t L, int64_t G, int S, float* sum_out,
-                     double* sum_out_f64) {
+                     double* sum_out_f64, unsigned* ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[RB_MAX_STAGES], empty[RB_MAX_STAGES];
+  __shared__ int64_t stage_row[RB_MAX_STAGES];
   const int W = S / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned row_bytes = (unsigned)(cols * 4);
@@ -152,11 +157,44 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
   if (warp == 0) {
     if (lane == 0) {
       int64_t k = 0;
-      for (int64_t r = blockIdx.x; r < rows; r += step, ++k) {
-        const int st = (int)(k % S);
-        if (k >= S) stage_acquire(&empty[st], (unsigned)(((k / S) - 1) & 1));
-        mbar_arrive_expect_tx(&full[st], row_bytes);
-        bulk_g2s(ring + st * stage_bytes, in + r * ld_in, row_bytes, &full[st]);
+      if (!ctr) {
+        for (int64_t r = blockIdx.x; r < rows; r += step, ++k) {
+          const int st = (int)(k % S);
+          if (k >= S) stage_acquire(&empty[st], (unsigned)(((k / S) - 1) & 1));
+          mbar_arrive_expect_tx(&full[st], row_bytes);
+          bulk_g2s(ring + st * stage_bytes, in + r * ld_in, row_bytes, &full[st]);
+        }
+      } else {
+        // rows [0, rs) grid-strided, then rows [rs, rows) from the queue, one
+        // claim ahead (a claim per row for every row capped the single producer
+        // at about one row per atomic round trip)
+        const int64_t dyn = rows * 3 / 100 > 8 * step ? rows * 3 / 100 : 8 * step;
+        const int64_t rs = rows > dyn ? rows - dyn : 0;
+        auto issue = [&](int64_t r) {
+          const int st = (int)(k % S);
+          if (k >= S) stage_acquire(&empty[st], (unsigned)(((k / S) - 1) & 1));
+          stage_row[st] = r;
+          mbar_arrive_expect_tx(&full[st], row_bytes);
+          bulk_g2s(ring + st * stage_bytes, in + r * ld_in, row_bytes, &full[st]);
+          ++k;
+        };
+        int64_t next = rs + (int64_t)atomicAdd(ctr, 1u);
+        for (int64_t r = blockIdx.x; r < rs; r += step) issue(r);
+        while (next < rows) {
+          const int64_t r = next;
+          next = rs + (int64_t)atomicAdd(ctr, 1u);
+          issue(r);
+        }
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every producer has claimed its last row
+          ctr[0] = 0u;
+          ctr[1] = 0u;
+        }
+        for (int j = 0; j < W; ++j, ++k) {  // end marker in each consumer warp's next stage
+          const int st = (int)(k % S);
+          if (k >= S) stage_acquire(&empty[st], (unsigned)(((k / S) - 1) & 1));
+          stage_row[st] = -1;
+          mbar_arrive(&full[st]);
+        }
       }
     }
     return;
@@ -164,10 +202,11 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
   const int w = warp - 1;
   const int nq = (int)(cols >> 2);  // float4s per row
   const bool vst = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) && (ld_out % 4 == 0);
-  for (int64_t k = w; blockIdx.x + k * step < rows; k += W) {
-    const int64_t r = blockIdx.x + k * step;
+  for (int64_t k = w; ctr || blockIdx.x + k * step < rows; k += W) {
     const int st = (int)(k % S);
     mbar_wait(&full[st], (unsigned)((k / S) & 1));
+    const int64_t r = ctr ? *(volatile int64_t*)&stage_row[st] : blockIdx.x + k * step;
+    if (r < 0) break;
     const float4* q = reinterpret_cast<const float4*>(ring + st * stage_bytes);
     double acc = 0.0;
     for (int j = lane; j < nq; j += 32) {
@@ -263,7 +302,7 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
       int64_t gb = d.sms;
       if (rows < gb) gb = rows;
       rows_bulk_kernel<<<(int)gb, 32 * (1 + S / 2), (size_t)S * stage_bytes, st>>>(
-          out, in, rows, cols, ld_out, ld_in, L, rc.G, S, sum_out, sum_out_f64);
+          out, in, rows, cols, ld_out, ld_in, L, rc.G, S, sum_out, sum_out_f64, rq);
       return cudaGetLastError();
     }
   }
