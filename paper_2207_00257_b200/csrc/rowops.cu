@@ -287,7 +287,7 @@ cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64
     const char* e = getenv("NORM_ROWS_QUEUE");
     return !(e && !strcmp(e, "0"));
   }();
-  unsigned* rq = queue ? row_ctr : nullptr;
+  unsigned* rq = queue && rows < (1ll << 31) ? row_ctr : nullptr;  // 32-bit claim counter
   const bool aligned = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 31u) == 0 &&
                        (ld_out % 8) == 0 && (ld_in % 8) == 0 && (cols % 8) == 0;
   const bool vec = aligned && out != in && cols <= (int64_t)SM_THREADS * 8 * 4;

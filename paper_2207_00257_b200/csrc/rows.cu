@@ -269,7 +269,7 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
     const char* e = getenv("NORM_ROWS_QUEUE");
     return !(e && !strcmp(e, "0"));
   }();
-  unsigned* rq = queue ? row_ctr : nullptr;
+  unsigned* rq = queue && rows < (1ll << 31) ? row_ctr : nullptr;  // 32-bit claim counter
   const int maxv = cols <= ROW_THREADS * 8 ? 1 : (cols <= ROW_THREADS * 16 ? 2 : 4);
   int64_t g = (int64_t)d.sms * row_ctas_per_sm(maxv);  // persistent: one wave
   if (rows < g) g = rows;
