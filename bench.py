@@ -810,6 +810,7 @@ def run_licm(args, world, rank, local):
     import paper_2207_00257_b200 as L
     stream = torch.cuda.current_stream()
     res = []
+    launches = 0
     for e in (10, 12, 14, 16, 18):
         n = 2**e
         inp = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -829,16 +830,39 @@ def run_licm(args, world, rank, local):
             b.record(stream)
             torch.cuda.synchronize()
             row[form + "_ms"] = a.elapsed_time(b) / reps
+            # the un-hoisted forms are one kernel; hoisted: one (small path) or reduce + scale
+            launches += reps * (2 if form == "hoisted" and n > 2**17 else 1)
         if "per_thread_ms" in row:
             row["per_thread_over_hoisted"] = row["per_thread_ms"] / row["hoisted_ms"]
         row["per_block_over_hoisted"] = row["per_block_ms"] / row["hoisted_ms"]
         res.append(row)
     last = res[-1]
+    # cpu_baseline leg of this workload: the oracle's three forms of Fig. 1 at
+    # BASELINE configs[0] (n = 1024, grid 32 x 32), with their exact add counts
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        x = gen.make_host(1024, seed=2207, dist="unit")
+        forms = {}
+        for name, fn in (("per_thread", oracle.form_thread), ("per_block", oracle.form_block),
+                         ("hoisted", oracle.form_hoisted)):
+            reps = 3
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                _, adds = fn(x, args.index)
+            forms[name] = {"ms": (time.perf_counter() - t0) / reps * 1e3, "adds": adds}
+        cpu = {"value": forms["per_thread"]["ms"] / forms["hoisted"]["ms"], "unit": "x (per-thread / hoisted, oracle, n=1024)",
+               "cores": 1, "kind": "oracle",
+               "sample": f"oracle forms of Fig. 1 at n=1024 ({args.index} index), 3 reps each, 1 thread of "
+                         f"{os.cpu_count()} ({cpu_model()}); adds = 32*G*n, G*n, n",
+               "forms": forms}
     line = {"metric": "Fig. 1 before/after parallel LICM on B200 (ms per call)",
             "value": last["per_block_over_hoisted"], "unit": "x (per-block / hoisted, n=2^18)",
             "n_gpus": 1, "steps": 5, "warmup": 2, "higher_is_better": True, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic", "config": {"workload": f"normalize_form, {args.index} index"},
-            "forms": res, "gpu_launches": None}
+            "forms": res, "gpu_launches": launches}
+    if cpu:
+        line["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(line), flush=True)
 
