@@ -131,7 +131,7 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(index, n_sample=2**28, reps=3):
+def oracle_sample(index, n_sample=2**28, reps=10):
     """Time the CPU oracle (form 3, hoisted O(N)) as it stands, single-threaded,
     on a bounded sample of the same workload; returns GB/s of algorithmic bytes."""
     import gen
