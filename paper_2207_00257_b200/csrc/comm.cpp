@@ -425,7 +425,7 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
   const int64_t Lloc = local_covered_prefix(mine, gcov);
   int path = o->path;
   if (path == NORM_PATH_AUTO) path = auto_path(local, Lloc, Lloc >= 0, d);
-  if (path == NORM_PATH_FUSED && Lloc > 0 && local > 0) {
+  if (path == NORM_PATH_FUSED && Lloc >= 0 && local > 0) {
     Coverage lc{};
     lc.kind = COV_PREFIX;
     lc.n = local;

@@ -1,0 +1,42 @@
+"""Host-side logic of bench.py (CPU): the local covered-prefix rule that picks
+the kernel the bench's roofline names must agree with the shard plans."""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import paper_2207_00257_b200 as L  # noqa: E402
+
+
+@pytest.mark.parametrize("n", [2**32, 2**28 + 77, 5000, 2**20 + 7])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_local_covered_prefix_matches_plans(n, world):
+    count, prefix = L.coverage(n, "literal")
+    for balanced in (True, False):
+        plan = L.plan_shards(n, world, "literal", balanced)
+        total = 0
+        for ranges in plan:
+            lloc = bench.local_covered_prefix(ranges, prefix)
+            covered = sum(max(0, min(b + ln, prefix) - b) for b, ln in ranges)
+            # literal coverage is a global prefix: every plan keeps it a local prefix
+            assert lloc == covered
+            total += covered
+        assert total == count
+    # dense: everything covered, the whole local buffer
+    _, dprefix = L.coverage(n, "dense")
+    for ranges in L.plan_shards(n, world, "dense", True):
+        assert bench.local_covered_prefix(ranges, dprefix) == sum(ln for _, ln in ranges)
+
+
+def test_local_covered_prefix_rejects_gaps():
+    # covered elements after uncovered ones (in local order) are not a local prefix
+    assert bench.local_covered_prefix([(100, 10), (0, 5)], 50) == -1
+    assert bench.local_covered_prefix([(0, 10), (20, 5)], 12) == 10  # 10, 11 live on another rank
+    # two fully covered ranges concatenate into one local prefix
+    assert bench.local_covered_prefix([(0, 10), (20, 5)], 50) == 15
+    assert bench.local_covered_prefix([(0, 10), (10, 5)], 12) == 12
+    assert bench.local_covered_prefix([(0, 4)], -1) == -1
