@@ -261,7 +261,7 @@ def run_vector(args, world, rank, local):
 
     n = args.n
     index = args.index
-    plan = L.plan_shards(n, world, index, True)
+    plan = L.plan_shards(n, world, index, args.plan == "balanced")
     mine = plan[rank]
     nloc = sum(ln for _, ln in mine)
     inp = torch.empty(max(nloc, 1), dtype=torch.float32, device="cuda")[:nloc]
@@ -448,6 +448,8 @@ def run_vector(args, world, rank, local):
                                   if world > 1 else ""),
                    "n": n, "index": index, "covered": cov_count, "algorithmic_bytes": algo,
                    "parallelism": f"shard{world}", "exchange": args.exchange if world > 1 else None,
+                   "shard_plan": (("coverage-balanced two-range" if args.plan == "balanced" else "uniform one-range")
+                                  if world > 1 else None),
                    "exchange_note": exchange_note, "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
                    "l2": f"no flush: {4 * nloc / 2**30:.1f} GiB input per GPU >> 126 MB L2"},
         "frac_of_hbm_peak": value / (world * peak),
@@ -878,6 +880,9 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
     ap.add_argument("--numel", dest="n", type=int, default=2**32)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--plan", default="balanced", choices=["balanced", "uniform"],
+                    help="N > 1 literal shard plan (SURVEY §8(e)): coverage-balanced two-range "
+                         "(default) or uniform one-range (rank 0 holds the whole covered prefix)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--also-dense", action="store_true", default=True)

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--index", default="literal")
     ap.add_argument("--numel", type=int, default=2**32)
     ap.add_argument("--only", type=int, default=0, help="run this W only (e.g. under ncu)")
+    ap.add_argument("--plan", default="balanced", choices=["balanced", "uniform"])
     args = ap.parse_args()
     n = args.numel
     torch.cuda.set_device(0)
@@ -43,7 +44,7 @@ def main():
     res = {}
     base = None
     for W in ((args.only,) if args.only else (1, 2, 4, 8)):
-        plan = L.plan_shards(n, W, args.index, True)
+        plan = L.plan_shards(n, W, args.index, args.plan == "balanced")
         ranks = sorted({0, W // 2, W - 1})
         per = {}
         for k in ranks:
@@ -76,7 +77,7 @@ def main():
         print(f"W={W}: per-rank ms {', '.join(f'r{k}={v:.4f}' for k, v in per.items())}  "
               f"-> {gbs:8.1f} GB/s aggregate, {gbs / (W * base):.3f} of W x one GPU", flush=True)
     pc.destroy()
-    print(json.dumps({"index": args.index, "n": n, "steps": args.steps, "results": res}))
+    print(json.dumps({"index": args.index, "plan": args.plan, "n": n, "steps": args.steps, "results": res}))
     dist.destroy_process_group()
 
 
