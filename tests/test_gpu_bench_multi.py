@@ -37,10 +37,12 @@ def _torchrun(args, timeout=600):
     return json.loads(lines[0]), r
 
 
-@pytest.mark.parametrize("exchange,n", [("p2p", 2**24 + 7), ("host", 2**24 + 7), ("p2p", 2**27 + 7)])
-def test_bench_vector_two_ranks(exchange, n):
+@pytest.mark.parametrize("exchange,n,plan", [("p2p", 2**24 + 7, "balanced"), ("host", 2**24 + 7, "balanced"),
+                                             ("p2p", 2**27 + 7, "balanced"), ("p2p", 2**27 + 7, "uniform")])
+def test_bench_vector_two_ranks(exchange, n, plan):
     d, r = _torchrun(["--numel", str(n), "--steps", "3", "--warmup", "3", "--exchange", exchange,
-                      "--e2e-steps", "1"])
+                      "--e2e-steps", "1", "--plan", plan])
+    assert d["config"]["shard_plan"].startswith("coverage-balanced" if plan == "balanced" else "uniform")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
               "clocks"):
