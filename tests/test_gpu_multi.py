@@ -84,6 +84,8 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
     (2, 2**20 + 7, "literal", False, "peer-fused"),  # one-range plan: rank 1 has nothing covered
     (2, 2**26 + 7, "literal", True, "peer"),  # AUTO picks fused per rank (local input > L2)
     (2, 2**26 + 7, "literal", True, "peer-2p"),
+    (8, 2**23 + 7, "literal", True, "peer-fused"),  # the 8-rank mailbox protocol (8 processes, one GPU)
+    (8, 2**23 + 7, "literal", True, "peer-2p"),
 ])
 def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange):
     import gen
