@@ -774,7 +774,7 @@ def run_backprop(args, world, rank, local):
     stream = torch.cuda.current_stream()
     nbytes = (16 * n_in * 4) * 2 + n_in * 4 * 2  # hidden read + write, input read, output write
     res = {}
-    for v in ("printed", "eliminated", "register"):
+    for v in ("printed", "eliminated", "register", "tma"):
         for _ in range(args.warmup):
             L.bpnn_layerforward(x, h, o, variant=v)
         times = []
@@ -790,15 +790,16 @@ def run_backprop(args, world, rank, local):
         res[v] = {"ms_per_step": ms, "value": nbytes / (ms / 1e3) / 1e9}
     peak, _ = load_peak()
     line = {"metric": "bpnn_layerforward GB/s (Rodinia backprop, Fig. backprop), in=2^22, hid=16",
-            "value": res["register"]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["register"]["ms_per_step"],
+            "value": res["tma"]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["tma"]["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": "norm_bpnn_layerforward in=2^22 hid=16",
                                             "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
-            "variants": res, "frac_of_hbm_peak": res["register"]["value"] / peak,
+            "variants": res, "frac_of_hbm_peak": res["tma"]["value"] / peak,
             "speedup_eliminated_over_printed": res["printed"]["ms_per_step"] / res["eliminated"]["ms_per_step"],
             "speedup_register_over_printed": res["printed"]["ms_per_step"] / res["register"]["ms_per_step"],
-            "gpu_launches": args.steps}
+            "speedup_tma_over_printed": res["printed"]["ms_per_step"] / res["tma"]["ms_per_step"],
+            "gpu_launches": args.steps * len(res)}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -201,7 +201,9 @@ norm_status_t norm_nll_backward(float* grad, const float* grad_out, const int64_
 typedef enum {
   NORM_BP_PRINTED = 0,     /* Fig. backprop as printed: shared memory, 8 barriers             */
   NORM_BP_ELIMINATED = 1,  /* §4.1/§4.2 by hand: barriers #1, #2 removed, store/load forwarded */
-  NORM_BP_REGISTER = 2     /* one thread per (block, column), tree in registers, 0 barriers    */
+  NORM_BP_REGISTER = 2,    /* one thread per (block, column), tree in registers, 0 barriers    */
+  NORM_BP_TMA = 3          /* REGISTER's arithmetic on tiles streamed by TMA (contiguous runs
+                              of 30 blocks, 4 x 32 KiB ring per SM, tiles from a queue)      */
 } norm_bp_variant_t;
 
 /* Rodinia backprop bpnn_layerforward (the kernel of Fig. backprop):

@@ -235,7 +235,7 @@ def nll_backward(grad_out, logp_shape, target, total_weight, weight=None, reduct
     return grad
 
 
-BP_VARIANT = {"printed": 0, "eliminated": 1, "register": 2}
+BP_VARIANT = {"printed": 0, "eliminated": 1, "register": 2, "tma": 3}
 
 
 def bpnn_layerforward(input_units, hidden, output, variant="register", stream=None):

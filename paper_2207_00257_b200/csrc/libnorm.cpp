@@ -143,6 +143,7 @@ Workspace workspace_carve(void* base) {
   w.task_ctr = w.ticket + 4;
   w.scale_ctr = w.ticket + 6;
   w.row_ctr = w.ticket + 8;
+  w.bp_ctr = w.ticket + 10;
   p += 256;
   w.task_sums = reinterpret_cast<double*>(p);
   return w;
@@ -707,7 +708,7 @@ NORM_API norm_status_t norm_bpnn_layerforward(const float* input, float* hidden,
                                               int64_t in, int64_t hid, int32_t variant,
                                               const norm_opts_t* o) {
   if (!o) o = &kDefaultOpts;
-  if (variant < NORM_BP_PRINTED || variant > NORM_BP_REGISTER)
+  if (variant < NORM_BP_PRINTED || variant > NORM_BP_TMA)
     return fail(NORM_ERR_INVALID_VALUE, "bad variant");
   if (in < 0) return fail(NORM_ERR_INVALID_VALUE, "in < 0");
   if (hid != 16 || in % 16 != 0)
@@ -718,8 +719,10 @@ NORM_API norm_status_t norm_bpnn_layerforward(const float* input, float* hidden,
   norm_status_t s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
+  Workspace ws;
+  if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_bpnn(input, hidden, output, in, hid, variant,
-                              static_cast<cudaStream_t>(o->stream));
+                              static_cast<cudaStream_t>(o->stream), d, ws.bp_ctr);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "bpnn kernel launch");
 }
 

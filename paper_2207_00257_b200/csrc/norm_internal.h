@@ -35,6 +35,7 @@ struct Workspace {
   unsigned* task_ctr;  // [1] next task of the bulk reduce's dynamic tail
   unsigned* scale_ctr; // [2] {next chunk, producers done} of the bulk scale's chunk queue
   unsigned* row_ctr;   // [2] {next row, CTAs done} of the register rows kernel's row queue
+  unsigned* bp_ctr;    // [2] {next tile run, producers done} of the TMA backprop kernel
   double* task_sums;   // [kMaxTasks] per-task sums of the dynamic tail
 };
 size_t workspace_bytes();
@@ -139,7 +140,7 @@ cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_
 
 // NEXT-4 backprop layerforward (backprop.cu)
 cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_t in, int64_t hid,
-                        int variant, cudaStream_t st);
+                        int variant, cudaStream_t st, const DeviceInfo& d, unsigned* ctr);
 
 // The AUTO path for a call over n elements whose covered set is [0, L) (prefix)
 // or not a prefix (libnorm.cpp; also used per rank by the sharded peer path).

@@ -1,4 +1,4 @@
-"""GPU parity for NEXT-4 (Rodinia bpnn_layerforward, Fig. backprop): all three
+"""GPU parity for NEXT-4 (Rodinia bpnn_layerforward, Fig. backprop): all four
 variants bitwise equal to the fp32 step-by-step oracle (same products, same tree
 order), in place on `hidden`, bias row/column untouched."""
 import numpy as np
@@ -12,8 +12,8 @@ import paper_2207_00257_b200 as L
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", ["printed", "eliminated", "register"])
-@pytest.mark.parametrize("n_in", [16, 64, 65536, 16 * 70001])
+@pytest.mark.parametrize("variant", ["printed", "eliminated", "register", "tma"])
+@pytest.mark.parametrize("n_in", [16, 32, 64, 16 * 31, 16 * 61, 65536, 16 * 70001])
 def test_bpnn_parity(variant, n_in):
     x = (gen.make_host(n_in + 1, seed=n_in, dist="signed")).astype(np.float32)
     w = (gen.make_host((n_in + 1) * 17, seed=n_in + 1, dist="wide").reshape(n_in + 1, 17) *
@@ -34,7 +34,7 @@ def test_bpnn_variants_agree_and_reject():
     x = torch.from_numpy(gen.make_host(n_in + 1, seed=1, dist="unit")).cuda()
     w0 = torch.from_numpy(gen.make_host((n_in + 1) * 17, seed=2, dist="unit").reshape(n_in + 1, 17)).cuda()
     res = []
-    for v in ("printed", "eliminated", "register"):
+    for v in ("printed", "eliminated", "register", "tma"):
         h = w0.clone()
         o = torch.empty(n_in, device="cuda")
         L.bpnn_layerforward(x, h, o, variant=v)
