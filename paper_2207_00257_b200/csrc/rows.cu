@@ -121,27 +121,27 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
 
 // Batched rows, TMA-staged, one WARP per row (rows of <= 48 KiB, 16-byte aligned
 // with cols % 4 == 0).  One CTA per SM: lane 0 of warp 0 streams whole rows
-// into a ring of S = 2W shared-memory stages with cp.async.bulk; consumer warp w
-// owns stages w and w + W and processes this CTA's rows k = w, w + W, ...: sum
+// into a ring of S shared-memory stages with cp.async.bulk; consumer warp w
+// (W warps, W divides S) owns stages w, w + W, ... and processes this CTA's
+// rows k = w, w + W, ...: sum
 // the row out of shared memory, warp-shuffle reduce (no block barrier on the
 // per-row critical path), then scale the covered elements out of shared memory
 // into `out`.  Up to S rows are in flight per SM, so HBM stays busy while each
 // warp finishes its row.
-constexpr int RB_MAX_STAGES = 16;
+constexpr int RB_MAX_STAGES = 16, RB_MAX_WARPS = 16;
 constexpr size_t RB_SMEM_BUDGET = 200 * 1024;
 
 // ctr != NULL: the producer takes its grid-strided share of the first 97 % of the
 // rows, then claims rows of the rest from a queue (one ahead), tagging each stage
 // with its row (stage_row); after the last row it posts an end marker to each
 // consumer warp's next stage; the last producer to run dry resets the queue.
-__global__ void __launch_bounds__(32 * (1 + RB_MAX_STAGES / 2), 1)
+__global__ void __launch_bounds__(32 * (1 + RB_MAX_WARPS), 1)
     rows_bulk_kernel(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
-                     int64_t ld_in, int64_t L, int64_t G, int S, float* sum_out,
+                     int64_t ld_in, int64_t L, int64_t G, int S, int W, float* sum_out,
                      double* sum_out_f64, unsigned* ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[RB_MAX_STAGES], empty[RB_MAX_STAGES];
   __shared__ int64_t stage_row[RB_MAX_STAGES];
-  const int W = S / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned row_bytes = (unsigned)(cols * 4);
   const size_t stage_bytes = ((size_t)row_bytes + 127) & ~(size_t)127;
@@ -291,6 +291,19 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
     int S = (int)(RB_SMEM_BUDGET / stage_bytes);
     if (S > RB_MAX_STAGES) S = RB_MAX_STAGES;
     S &= ~1;
+    // Consumer warps: warp w takes rows k = w, w + W, ... in stage k % S, and its
+    // mbarrier parity waits are only safe if the previous use of that stage was
+    // its own (so it has landed): W must divide S.  One stage per warp (W = S)
+    // measured best for 16 KiB rows (204 vs 209 us with W = S / 2); W = 8 with
+    // S = 12 aliased phases and read stale rows.  NORM_ROWS_BULK_WARPS: A/B knob,
+    // honoured only if it divides S.
+    static const int warps_env = [] {
+      const char* e = getenv("NORM_ROWS_BULK_WARPS");
+      return e ? atoi(e) : 0;
+    }();
+    int W = S;
+    if (warps_env > 0 && S % warps_env == 0) W = warps_env;
+    if (W > RB_MAX_WARPS) W = RB_MAX_WARPS;
     if (S >= 2) {
       static int configured[64] = {0};
       if (d.device < 64 && !configured[d.device]) {
@@ -301,8 +314,8 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
       }
       int64_t gb = d.sms;
       if (rows < gb) gb = rows;
-      rows_bulk_kernel<<<(int)gb, 32 * (1 + S / 2), (size_t)S * stage_bytes, st>>>(
-          out, in, rows, cols, ld_out, ld_in, L, rc.G, S, sum_out, sum_out_f64, rq);
+      rows_bulk_kernel<<<(int)gb, 32 * (1 + W), (size_t)S * stage_bytes, st>>>(
+          out, in, rows, cols, ld_out, ld_in, L, rc.G, S, W, sum_out, sum_out_f64, rq);
       return cudaGetLastError();
     }
   }

@@ -659,3 +659,22 @@ def test_dynamic_tail_deterministic(offset, path):
                 Sx = oracle.sum_exact(xs)
                 assert abs(ref - Sx) <= 1e-6 * oracle.sum_abs_exact(xs)
             assert S.item() == ref
+
+
+@pytest.mark.parametrize("cols", [512, 1024, 2048, 4096, 8192, 12288])
+def test_rows_bulk_stage_geometries(cols):
+    """The TMA warp-per-row kernel at row sizes that give 4..16 ring stages (one
+    consumer warp per stage): every row of a literal batch replayed bitwise."""
+    R = 777
+    x = gen.make_host(R * cols, seed=cols, dist=0).reshape(R, cols)
+    inp = to_dev(x)
+    out = to_dev(sentinel(R * cols).reshape(R, cols))
+    s = torch.zeros(R, device="cuda")
+    L.normalize_rows(out, inp, index="literal", sum_out=s)
+    torch.cuda.synchronize()
+    o, sv = out.cpu().numpy(), s.cpu().numpy()
+    for r in range(R):
+        S = oracle.sum_exact(x[r])
+        assert abs(float(sv[r]) - S) <= 1e-6 * S
+        rep = oracle.replay(x[r], sv[r], "literal", out=sentinel(cols))
+        assert o[r].view(np.uint32).tobytes() == rep.view(np.uint32).tobytes(), r
