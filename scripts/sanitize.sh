@@ -30,6 +30,14 @@ L.softmax_rows(y, x); L.softmax_rows(y, x, log=True)
 t = (torch.rand(64, device="cuda") * 2048).long()
 loss, tw = L.nll_forward(y, t)
 g = L.nll_backward(torch.ones(1, device="cuda"), (64, 2048), t, tw)
+for v in ("printed", "eliminated", "register", "tma"):
+    for n_in in (16, 32, 16 * 61, 16 * 4001):
+        xi = torch.rand(n_in + 1, device="cuda"); hw = torch.rand(n_in + 1, 17, device="cuda")
+        ob = torch.empty(n_in, device="cuda")
+        L.bpnn_layerforward(xi, hw, ob, variant=v)
+for C in (512, 1024, 8192, 12288):
+    x = torch.rand(37, C, device="cuda"); y = torch.zeros_like(x)
+    L.normalize_rows(y, x, index="literal")
 h = torch.rand(2**20 + 7).pin_memory(); o = torch.zeros_like(h).pin_memory()
 L.normalize_host(o, h)
 torch.cuda.synchronize()
