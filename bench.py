@@ -218,6 +218,13 @@ def barrier(world):
 
 
 
+def workload_name(n, index):
+    """The workload key shared by both arms' JSON lines."""
+    e = n.bit_length() - 1
+    size = f"2^{e}" if n == 1 << e else str(n)
+    return f"normalize n={size} fp32 (Fig. 1), {index} index"
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -244,9 +251,10 @@ def run_reference(args):
         "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"normalize n=2^32 fp32 (Fig. 1), {args.index} index",
-                   "sample": f"CPU oracle (form 3, hoisted) on a bounded sample: n={n_sample} per step",
-                   "n": n_sample, "index": args.index},
+        "config": {"workload": workload_name(args.n, args.index),
+                   "sample": f"CPU oracle (form 3, hoisted) on a bounded sample: n={n_sample} per step; "
+                             f"value = the sample's algorithmic bytes / its time",
+                   "n": args.n, "sample_n": n_sample, "index": args.index},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
                          "sample": f"n={n_sample} per step, 1 thread of {os.cpu_count()} ({cpu_model()})"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -439,13 +447,12 @@ def run_vector(args, world, rank, local):
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"normalize n=2^{n.bit_length() - 1} fp32 (Fig. 1), {index} index, "
-                               f"{'two-pass' if world > 1 or args.path == 'auto' else args.path}"
-                               + ((", coverage-balanced shards + 8 B " + {
-                                   "nccl": "ncclAllGather", "nccl-allreduce": "ncclAllReduce",
-                                   "p2p": "peer-memory stores from the reduce kernel",
-                                   "host": "all-gather over the torch.distributed group"}[args.exchange])
-                                  if world > 1 else ""),
+        "config": {"workload": workload_name(n, index),
+                   "path": kpath + (" per rank" if world > 1 else ""),
+                   "exchange_desc": ("8 B per rank: " + {
+                       "nccl": "ncclAllGather", "nccl-allreduce": "ncclAllReduce",
+                       "p2p": "peer-memory stores into every rank's mailbox from the reduce / fused kernel",
+                       "host": "all-gather over the torch.distributed group"}[args.exchange]) if world > 1 else None,
                    "n": n, "index": index, "covered": cov_count, "algorithmic_bytes": algo,
                    "parallelism": f"shard{world}", "exchange": args.exchange if world > 1 else None,
                    "shard_plan": (("coverage-balanced two-range" if args.plan == "balanced" else "uniform one-range")
