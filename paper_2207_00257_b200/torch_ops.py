@@ -8,6 +8,7 @@ the dispatcher, autograd-opaque and traceable by torch.compile:
     torch.ops.libnorm.normalize(x, index="dense")       -> Tensor
     torch.ops.libnorm.normalize_rows(x, index="dense")  -> Tensor   (2-D, per row)
     torch.ops.libnorm.normalize_(x, index="literal")    -> None     (in place)
+    torch.ops.libnorm.softmax(x, log=False)              -> Tensor   (2-D, per row; NEXT-2)
 
 Functional forms return a fresh tensor whose covered elements are x[i] / s and
 whose uncovered elements (literal index, reading R1) are copies of x — i.e. the
@@ -62,6 +63,24 @@ def normalize_(x: torch.Tensor, index: str = "literal") -> None:
     if not x.is_contiguous():
         raise RuntimeError("libnorm::normalize_ needs a contiguous tensor")
     _lib.normalize(x, x, index=index)
+
+
+@torch.library.custom_op("libnorm::softmax", mutates_args=())
+def softmax(x: torch.Tensor, log: bool = False) -> torch.Tensor:
+    """Row softmax / log-softmax of a 2-D tensor (norm_softmax_rows): the
+    "aggregation operations like Softmax" the paper transpiles."""
+    _check(x)
+    if x.dim() != 2:
+        raise RuntimeError("libnorm::softmax expects a 2-D tensor")
+    src = x.contiguous()
+    out = torch.empty_like(src)
+    _lib.softmax_rows(out, src, log=log)
+    return out
+
+
+@softmax.register_fake
+def _(x, log=False):
+    return torch.empty_like(x, memory_format=torch.contiguous_format)
 
 
 class Normalize(torch.nn.Module):

@@ -470,6 +470,14 @@ def test_torch_ops():
     assert torch.allclose(f(m), r, rtol=1e-6, atol=0)
     with pytest.raises(RuntimeError):
         torch.ops.libnorm.normalize(torch.ones(4), "dense")
+    # NEXT-2 kernels through the dispatcher (tolerances of DESIGN.md §9)
+    lg = to_dev(gen.make_host(96 * 4096, seed=5, dist=3).reshape(96, 4096)) * 8
+    sm = torch.ops.libnorm.softmax(lg, False)
+    ls = torch.ops.libnorm.softmax(lg, True)
+    assert torch.allclose(sm, torch.softmax(lg.double(), 1).float(), rtol=1e-5, atol=1e-37)
+    assert torch.allclose(ls, torch.log_softmax(lg.double(), 1).float(), rtol=1e-5, atol=1e-5)
+    g = torch.compile(lambda t: torch.ops.libnorm.softmax(t, False), fullgraph=True)
+    assert torch.equal(g(lg), sm)
 
 
 def test_signed_zeros_and_zero_heavy():
