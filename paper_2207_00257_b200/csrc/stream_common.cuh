@@ -114,14 +114,18 @@ __device__ __forceinline__ void scale_segment(float* out, const float* in, int64
 // carries across segments, so a kernel can stream several segments in a row.
 constexpr int BK_CONSUMERS = 256, BK_THREADS = BK_CONSUMERS + 32;
 constexpr int BK_STAGES = 4, BK_CHUNK = 32768;  // reduce: 4 x 32 KiB in flight per SM
-constexpr int SB_STAGES = 2, SB_CHUNK = 49152;  // scale: 2 x 48 KiB (loads share HBM with stores)
+#ifndef NORM_SB_STAGES  // probe builds may override (scripts/ab_libs.py)
+#define NORM_SB_STAGES 2
+#define NORM_SB_CHUNK 49152
+#endif
+constexpr int SB_STAGES = NORM_SB_STAGES, SB_CHUNK = NORM_SB_CHUNK;  // scale: 2 x 48 KiB (loads share HBM with stores)
 constexpr size_t BK_SMEM = (size_t)BK_STAGES * BK_CHUNK;
 // The scale ring uses 96 KiB but reserves 116 KiB (> half of the SM's 228 KiB):
 // exactly one scale CTA fits per SM, so its persistent grid spreads one CTA per
 // SM even when PDL launches it while reduce CTAs are still resident (without
 // the reservation two scale CTAs can land on one SM: measured 0.5 ms slower on
 // dense 2^32).
-constexpr size_t SB_SMEM = 116 * 1024;
+constexpr size_t SB_SMEM = (size_t)SB_STAGES * SB_CHUNK > 116 * 1024 ? (size_t)SB_STAGES * SB_CHUNK : 116 * 1024;
 static_assert((size_t)SB_STAGES * SB_CHUNK <= SB_SMEM, "ring fits the reservation");
 constexpr int64_t kBulkMinN = 1 << 22;  // below this the LDG kernels are as fast
 

@@ -17,4 +17,4 @@ for r in range(reps):
         env = dict(os.environ, LIBNORM_SO=os.path.abspath(so))
         out = subprocess.run(cmd, env=env, capture_output=True, text=True).stdout
         for line in out.strip().splitlines():
-            print(f"[{tag} rep{r}] {line[:300]}", flush=True)
+            print(f"[{tag} rep{r}] {line}", flush=True)
