@@ -686,3 +686,35 @@ def test_rows_bulk_stage_geometries(cols):
         assert abs(float(sv[r]) - S) <= 1e-6 * S
         rep = oracle.replay(x[r], sv[r], "literal", out=sentinel(cols))
         assert o[r].view(np.uint32).tobytes() == rep.view(np.uint32).tobytes(), r
+
+
+@pytest.mark.parametrize("dist_kind,mode", [(4, "literal"), (3, "dense")])
+def test_large_wide_and_signed_2_30(dist_kind, mode):
+    """n = 2^30 through the bulk reduce (dynamic tail) and the scale queue with
+    wide-exponent (D4, 2^-32..2^31) and signed (D3, cancellation) inputs: s within
+    1e-6 of the exact sum (relative to sum|x| for D3), sampled bitwise replay,
+    and run-to-run identical bits."""
+    n = 2**30
+    inp = torch.empty(n, dtype=torch.float32, device="cuda")
+    gen.fill_cuda(inp, seed=31, dist=dist_kind)
+    out = torch.empty_like(inp)
+    s = torch.zeros(1, device="cuda")
+    S64 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    L.normalize(out, inp, index=mode, path="two_pass", sum_out=s, sum_out_f64=S64)
+    torch.cuda.synchronize()
+    x = inp.cpu().numpy()
+    S = oracle.sum_exact(x)
+    scale = oracle.sum_abs_exact(x) if dist_kind == 3 else abs(S)
+    sv = np.float32(s.item())
+    assert abs(float(sv) - S) <= 1e-6 * scale
+    count, prefix = oracle.coverage_closed(n, mode)
+    rng = np.random.default_rng(7)
+    idx = rng.integers(0, prefix, 1 << 21)
+    o = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+    with np.errstate(all="ignore"):
+        rep = (x[idx] / sv).astype(np.float32)
+    assert np.array_equal(o.view(np.uint32), rep.view(np.uint32))
+    S2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    L.normalize(out, inp, index=mode, path="two_pass", sum_out_f64=S2)
+    torch.cuda.synchronize()
+    assert S2.item() == S64.item()
