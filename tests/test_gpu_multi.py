@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
+def _worker(rank, world, port, n, mode, balanced, q, exchange="gather", values="unit"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import gen
@@ -39,7 +39,7 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
         inp = torch.empty(max(nloc, 1), device="cuda")[:nloc]
         off = 0
         for b, ln in ranges:
-            gen.fill_cuda(inp[off:off + ln], seed=11, dist="unit", offset=b)
+            gen.fill_cuda(inp[off:off + ln], seed=11, dist=values, offset=b)
             off += ln
         out = torch.full((nloc,), -5.0, device="cuda")
         s = torch.zeros(1, device="cuda")
@@ -56,12 +56,18 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
             ref = torch.full((nloc,), -5.0, device="cuda")
             sref = torch.zeros(1, device="cuda")
             L.normalize_sharded_via(ref, inp, ranges, n, ag, index=mode, sum_out=sref)
-            path = "fused" if exchange == "peer-fused" else ("two_pass" if exchange == "peer-2p" else "auto")
+            path = "fused" if exchange.startswith("peer-fused") else ("two_pass" if exchange == "peer-2p" else "auto")
+            first = None
             for _ in range(7):
                 out.fill_(-5.0)
                 pc.normalize_sharded(out, inp, ranges, n, index=mode, sum_out=s, path=path)
                 torch.cuda.synchronize()
-                assert torch.equal(out, ref) and torch.equal(s, sref)
+                if values == "unit":  # grid values: every summation order gives the same bits
+                    assert torch.equal(out, ref) and torch.equal(s, sref)
+                elif first is None:
+                    first = (out.clone(), s.clone())
+                else:  # other inputs: the fused partial's order differs from the gathered one,
+                    assert torch.equal(out, first[0]) and torch.equal(s, first[1])  # but repeats
             dist.barrier()
             pc.destroy()
         torch.cuda.synchronize()
@@ -70,30 +76,33 @@ def _worker(rank, world, port, n, mode, balanced, q, exchange="gather"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,mode,balanced,exchange", [
-    (2, 2**20 + 7, "literal", True, "gather"),
-    (3, 2**20 + 7, "literal", False, "gather"),
-    (4, 3 * 2**20 + 5, "dense", True, "gather"),
-    (2, 700, "literal", True, "gather"),
-    (2, 2**22 + 7, "literal", True, "peer"),
-    (4, 3 * 2**20 + 5, "dense", True, "peer"),
-    (3, 700, "literal", True, "peer"),  # ranks without covered elements still wait every epoch
+@pytest.mark.parametrize("world,n,mode,balanced,exchange,values", [
+    (2, 2**20 + 7, "literal", True, "gather", "unit"),
+    (3, 2**20 + 7, "literal", False, "gather", "unit"),
+    (4, 3 * 2**20 + 5, "dense", True, "gather", "unit"),
+    (2, 700, "literal", True, "gather", "unit"),
+    (2, 2**22 + 7, "literal", True, "peer", "unit"),
+    (4, 3 * 2**20 + 5, "dense", True, "peer", "unit"),
+    (3, 700, "literal", True, "peer", "unit"),  # ranks without covered elements still wait every epoch
     # one fused kernel per rank (reduce, grid barrier, publish + mailbox wait, scale)
-    (2, 2**22 + 7, "literal", True, "peer-fused"),
-    (3, 3 * 2**20 + 5, "dense", True, "peer-fused"),
-    (2, 2**20 + 7, "literal", False, "peer-fused"),  # one-range plan: rank 1 has nothing covered
-    (2, 2**26 + 7, "literal", True, "peer"),  # AUTO picks fused per rank (local input > L2)
-    (2, 2**26 + 7, "literal", True, "peer-2p"),
-    (8, 2**23 + 7, "literal", True, "peer-fused"),  # the 8-rank mailbox protocol (8 processes, one GPU)
-    (8, 2**23 + 7, "literal", True, "peer-2p"),
+    (2, 2**22 + 7, "literal", True, "peer-fused", "unit"),
+    (3, 3 * 2**20 + 5, "dense", True, "peer-fused", "unit"),
+    (2, 2**20 + 7, "literal", False, "peer-fused", "unit"),  # one-range plan: rank 1 has nothing covered
+    (2, 2**26 + 7, "literal", True, "peer", "unit"),  # AUTO picks fused per rank (local input > L2)
+    (2, 2**26 + 7, "literal", True, "peer-2p", "unit"),
+    (8, 2**23 + 7, "literal", True, "peer-fused", "unit"),  # the 8-rank mailbox protocol (8 processes, one GPU)
+    (8, 2**23 + 7, "literal", True, "peer-2p", "unit"),
+    # wide-exponent inputs: s bit-identical on every rank and run, within 1e-6 of the exact sum
+    (3, 2**23 + 7, "literal", True, "peer-fused", "wide"),
+    (4, 2**22 + 9, "dense", True, "peer-fused", "wide"),
 ])
-def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange):
+def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange, values):
     import gen
     import oracle
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, n, mode, balanced, q, exchange))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, mode, balanced, q, exchange, values))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -104,7 +113,7 @@ def test_sharded_ranks_on_one_gpu(world, n, mode, balanced, exchange):
     svals = {r[2] for r in res}
     assert len(svals) == 1  # bit-identical divisor on every rank
     sv = np.float32(res[0][2])
-    x = gen.make_host(n, seed=11, dist="unit")
+    x = gen.make_host(n, seed=11, dist=values)
     S = oracle.sum_exact(x)
     assert abs(float(sv) - S) <= 1e-6 * S
     full = np.full(n, -5.0, np.float32)
