@@ -156,7 +156,9 @@ norm_status_t norm_launch_form(float* out, const float* in, int64_t n, int32_t f
 /* Batched per-row variant (reading R10; BASELINE configs[4]): for each row r,
  * out[r*ld_out + i] = in[r*ld_in + i] / s_r for i in C(cols), s_r ~ sum of row r.
  * Row r is exactly norm_launch_ex(out + r*ld_out, in + r*ld_in, cols, o).
- * o->sum_out / sum_out_f64, when set, receive one value per row. */
+ * o->sum_out / sum_out_f64, when set, receive one value per row.  o->workspace
+ * holds the row queue (CTAs take rows dynamically; each row's result does not
+ * depend on which CTA computes it). */
 norm_status_t norm_rows(float* out, const float* in, int64_t rows, int64_t cols,
                         int64_t ld_out, int64_t ld_in, const norm_opts_t* o);
 
@@ -202,8 +204,8 @@ typedef enum {
   NORM_BP_PRINTED = 0,     /* Fig. backprop as printed: shared memory, 8 barriers             */
   NORM_BP_ELIMINATED = 1,  /* §4.1/§4.2 by hand: barriers #1, #2 removed, store/load forwarded */
   NORM_BP_REGISTER = 2,    /* one thread per (block, column), tree in registers, 0 barriers    */
-  NORM_BP_TMA = 3          /* REGISTER's arithmetic on tiles streamed by TMA (contiguous runs
-                              of 30 blocks, 4 x 32 KiB ring per SM, tiles from a queue)      */
+  NORM_BP_TMA = 3          /* REGISTER's arithmetic on tiles streamed by TMA (runs of 15
+                              blocks + their inputs, 4-stage ring, 2 CTAs/SM, run queue)     */
 } norm_bp_variant_t;
 
 /* Rodinia backprop bpnn_layerforward (the kernel of Fig. backprop):
@@ -214,7 +216,7 @@ typedef enum {
  * input: device fp32[in + 1]; hidden: device fp32[(in + 1) * (hid + 1)], updated in
  * place as the Rodinia kernel does; output: device fp32[in].  hid must be 16 and in a
  * multiple of 16 (else NORM_ERR_UNSUPPORTED).  All variants are bitwise identical
- * (reading R18).  o->stream is used. */
+ * (reading R18).  o->stream and o->workspace (the TMA form's run queue) are used. */
 norm_status_t norm_bpnn_layerforward(const float* input, float* hidden, float* output, int64_t in,
                                      int64_t hid, int32_t variant, const norm_opts_t* o);
 
