@@ -254,14 +254,24 @@ __global__ void __launch_bounds__(256)
                         int reduction, int64_t ignore_index) {
   const double tw = reduction == NORM_REDUCTION_MEAN ? (double)*total_weight : 1.0;
   const double g0 = reduction == NORM_REDUCTION_NONE ? 0.0 : (double)grad_out[0];
-  for (int64_t r = blockIdx.x; r < N; r += gridDim.x) {
-    const int64_t t = target[r];
+  // the next row's target (and grad_out) are loaded one row ahead, so the row's
+  // write stream does not wait on a dependent load each time
+  int64_t r = blockIdx.x;
+  int64_t t_next = r < N ? target[r] : 0;
+  double go_next = (reduction == NORM_REDUCTION_NONE && r < N) ? (double)grad_out[r] : g0;
+  for (; r < N; r += gridDim.x) {
+    const int64_t t = t_next;
+    const double go = go_next;
+    const int64_t rn = r + gridDim.x;
+    if (rn < N) {
+      t_next = target[rn];
+      if (reduction == NORM_REDUCTION_NONE) go_next = (double)grad_out[rn];
+    }
     const bool hit = t != ignore_index && t >= 0 && t < C;
     float val = 0.0f;
     if (hit) {
       const double w = weight ? (double)weight[t] : 1.0;
-      const double g = reduction == NORM_REDUCTION_NONE ? (double)grad_out[r] : g0;
-      val = (float)(-w * g / tw);
+      val = (float)(-w * go / tw);
     }
     float* row = grad + r * ld;
     if constexpr (VEC) {
