@@ -154,6 +154,17 @@ def oracle_sample(index, n_sample=2**28, reps=10):
 
 # --------------------------------------------------------------------------- arms
 
+def _wait_for_cuda(timeout_s=90):
+    """A freshly handed-over box can briefly refuse CUDA initialisation, and the
+    CUDA runtime caches that failure per process: probe in subprocesses first."""
+    probe = [sys.executable, "-c", "import torch, sys; sys.exit(0 if torch.cuda.is_available() else 1)"]
+    deadline = time.time() + timeout_s
+    while time.time() < deadline:
+        if subprocess.run(probe, capture_output=True).returncode == 0:
+            return
+        time.sleep(5)
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -904,6 +915,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    _wait_for_cuda()
     world, rank, local = dist_setup(args)
     try:
         if args.workload == "vector":
