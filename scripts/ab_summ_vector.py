@@ -1,3 +1,5 @@
+"""Summarise ab_libs.py / ab_env.sh lines '[tag] {bench json}' of the vector
+workload: literal and dense step times (probe, not product)."""
 import sys, json
 for line in sys.stdin:
     if not line.startswith("["): continue

@@ -1,3 +1,5 @@
+"""Pinned host -> device copy rate with 1, 2, 4 concurrent streams, and H2D with a
+concurrent D2H (probe, not product): the link the e2e number is bound by."""
 import torch, time
 n = 1 << 30  # 4 GiB fp32
 h = torch.empty(n, dtype=torch.float32, pin_memory=True)
