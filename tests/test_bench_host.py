@@ -40,3 +40,22 @@ def test_local_covered_prefix_rejects_gaps():
     assert bench.local_covered_prefix([(0, 10), (20, 5)], 50) == 15
     assert bench.local_covered_prefix([(0, 10), (10, 5)], 12) == 12
     assert bench.local_covered_prefix([(0, 4)], -1) == -1
+
+
+def test_reference_arm_json_contract():
+    """`bench.py --impl reference` (the oracle on the host cores) prints one JSON
+    line with the libnorm arm's metric, unit, direction and workload name."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["metric"] == "normalize GB/s and % of HBM peak, n=2^32 fp32, at 1/2/4/8 B200"
+    assert d["unit"] == "GB/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["config"]["workload"] == bench.workload_name(2**32, "literal")
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
