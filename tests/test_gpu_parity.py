@@ -669,7 +669,7 @@ def test_dynamic_tail_deterministic(offset, path):
             assert S.item() == ref
 
 
-@pytest.mark.parametrize("cols", [512, 1024, 2048, 4096, 8192, 12288])
+@pytest.mark.parametrize("cols", [256, 384, 512, 1024, 2048, 4096, 8192, 12288])
 def test_rows_bulk_stage_geometries(cols):
     """The TMA warp-per-row kernel at row sizes that give 4..16 ring stages (one
     consumer warp per stage): every row of a literal batch replayed bitwise."""
