@@ -286,7 +286,11 @@ cudaError_t launch_rows(float* out, const float* in, int64_t rows, int64_t cols,
   const bool bulk_ok = ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) && (ld_in % 4) == 0 &&
                        (cols % 4) == 0 && cols * 4 <= 48 * 1024 && cols >= 256 &&
                        covered * 2 <= cols;
-  if (bulk_ok && !getenv("NORM_ROWS_NO_BULK")) {
+  static const bool no_bulk = [] {  // A/B knob: NORM_ROWS_NO_BULK=1 forces the register kernel
+    const char* e = getenv("NORM_ROWS_NO_BULK");
+    return e && strcmp(e, "0") != 0 && e[0] != '\0';
+  }();
+  if (bulk_ok && !no_bulk) {
     const size_t stage_bytes = ((size_t)cols * 4 + 127) & ~(size_t)127;
     int S = (int)(RB_SMEM_BUDGET / stage_bytes);
     if (S > RB_MAX_STAGES) S = RB_MAX_STAGES;
