@@ -9,7 +9,6 @@
 
 namespace lnorm {
 
-
 #ifdef NORM_TIMELINE  // probe builds only (scripts/fused_timeline.py): per-CTA %globaltimer stamps
 __device__ unsigned long long g_fused_ts[4096 * 5];
 __device__ __forceinline__ unsigned long long stamp_ns() {  // ordered with memory ops
@@ -23,30 +22,28 @@ __device__ __forceinline__ unsigned long long stamp_ns() {  // ordered with memo
 #define FUSED_STAMP(k)
 #endif
 
-// ---------------------------------------------------------------- fused
-// Grid-wide barrier of a cooperative launch (one per kernel): bar = {count,
-// generation}.  Each CTA's thread 0 read the generation at kernel start (`gen`;
-// it only changes at this barrier), arrives with an acq_rel add (its CTA's prior
-// writes released; the last arriver acquires everyone's); the last arriver
-// resets the count and publishes gen + 1 with a release store; the others spin
-// on an acquire load of the generation.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned gen) {
+// Grid barrier by arrival count (one per kernel): `arrivals` only grows — each
+// CTA's thread 0 adds 1 with a release reduction (no round trip) and spins on an
+// acquire load until the count reaches this barrier's target, the next multiple
+// of the grid size above the value it read at kernel start (that value is at
+// least the previous barriers' total and below it plus one grid: no CTA of this
+// kernel can complete the barrier before this one arrives).  The last arrival's
+// add itself releases everyone (acquire of the final value synchronises with
+// every CTA's release through the RMW chain).  64-bit: no wrap in practice.
+__device__ __forceinline__ void grid_barrier_count(unsigned long long* arrivals, unsigned long long target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (atom_add_acq_rel_u32(bar, 1u) == gridDim.x - 1) {
-      st_relaxed_u32(bar, 0u);
-      st_release_u32(bar + 1, gen + 1u);
-    } else {
-      while (ld_acquire_u32(bar + 1) == gen) {
-      }
+    red_add_release_u64(arrivals, 1ull);
+    while (ld_acquire_u64(arrivals) < target) {
     }
 #ifdef NORM_TIMELINE
-    g_fused_ts[blockIdx.x * 5 + 2] = stamp_ns();  // thread 0 out of the spin
+    g_fused_ts[blockIdx.x * 5 + 2] = stamp_ns();
 #endif
   }
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- fused
 // Single pass: one cooperative CTA per SM streams the uncovered
 // tail [L, n) through the TMA-bulk ring, then the covered prefix [0, L) (read
 // LAST, with an L2 evict_last hint, so as much of it as fits is still in L2);
@@ -63,15 +60,17 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned gen) {
 template <bool VEC>
 __global__ void __launch_bounds__(BK_THREADS, 1)
     fused_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials,
-                 unsigned* bar, float* sum_out, double* sum_out_f64, int hints, PeerPost post,
-                 const double* mailbox, unsigned* task_ctr, double* task_sums, int64_t dyn, int tc) {
+                 float* sum_out, double* sum_out_f64, int hints, PeerPost post,
+                 const double* mailbox, unsigned* task_ctr, double* task_sums, int64_t dyn, int tc,
+                 unsigned long long* arrivals) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
   __shared__ DynSmem dsm;
   __shared__ double red[BK_THREADS / 32];
   __shared__ double S_sh;
   FUSED_STAMP(0)
-  const unsigned gen = threadIdx.x == 0 ? ld_acquire_u32(bar + 1) : 0u;  // grid_barrier's generation
+  unsigned long long target = 0;  // grid_barrier_count's target
+  if (threadIdx.x == 0) target = (ld_acquire_u64(arrivals) / gridDim.x + 1) * gridDim.x;
   if (threadIdx.x < 2) dsm.slot_cnt[threadIdx.x] = 0u;
   auto r = bulk_ring_init<BK_STAGES, BK_CHUNK>(ring, full, empty);
   // phase 1: the tail, then the covered prefix (read last), with a dynamic,
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   FUSED_STAMP(1)
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
-  grid_barrier(bar, gen);  // all of `in` has been read: `out` (possibly == in) may be written
+  grid_barrier_count(arrivals, target);  // all of `in` has been read: `out` (possibly == in) may be written
   if (blockIdx.x == 0 && threadIdx.x == 0) *task_ctr = 0u;  // every CTA is done claiming
   double v = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += BK_THREADS) v += __ldcg(partials + i);
@@ -145,15 +144,15 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
   int grid = d.sms;  // one CTA per SM
   int64_t n = cov.n, L = cov.L;
   double* partials = ws.partials;
-  unsigned* bar = ws.bar;
   int hints = fused_hints(cov, d);
   unsigned* task_ctr = ws.task_ctr;
   double* task_sums = ws.task_sums;
   int tc = 0;
   int64_t dyn = dyn_chunks(n, grid, &tc);
   if (tc < kDynMinTC) tc = kDynMinTC;
-  void* args[] = {&out, (void*)&in, &n, &L, &partials, &bar, &sum_out, &sum_out_f64, &hints,
-                  &post, (void*)&mailbox, &task_ctr, &task_sums, &dyn, &tc};
+  unsigned long long* arrivals = ws.arrivals;
+  void* args[] = {&out, (void*)&in, &n, &L, &partials, &sum_out, &sum_out_f64, &hints,
+                  &post, (void*)&mailbox, &task_ctr, &task_sums, &dyn, &tc, &arrivals};
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BK_THREADS), args, BK_SMEM, st);
 }
 

@@ -127,7 +127,7 @@ static norm_status_t check_device(DeviceInfo* d) {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 size_t workspace_bytes() {
-  return align_up(kMaxGrid * sizeof(double), 256) + 256 /* S[4] */ + 256 /* ticket, bar, task_ctr */ +
+  return align_up(kMaxGrid * sizeof(double), 256) + 256 /* S[4] */ + 256 /* ticket and the queue / barrier counters */ +
          align_up(kMaxTasks * sizeof(double), 256);
 }
 
@@ -139,11 +139,11 @@ Workspace workspace_carve(void* base) {
   w.S = reinterpret_cast<double*>(p);
   p += 256;
   w.ticket = reinterpret_cast<unsigned*>(p);
-  w.bar = w.ticket + 1;
   w.task_ctr = w.ticket + 4;
   w.scale_ctr = w.ticket + 6;
   w.row_ctr = w.ticket + 8;
   w.bp_ctr = w.ticket + 10;
+  w.arrivals = reinterpret_cast<unsigned long long*>(w.ticket + 12);  // 8-byte aligned
   p += 256;
   w.task_sums = reinterpret_cast<double*>(p);
   return w;

@@ -31,11 +31,11 @@ struct Workspace {
   double* partials;    // [kMaxGrid] per-CTA partial sums
   double* S;           // [4] fp64 sum slots (S[0]: vector sum; S[1]: sharded local partial)
   unsigned* ticket;    // [1] last-block ticket of the reduce kernel
-  unsigned* bar;       // [2] grid barrier {count, generation} of the fused kernel
   unsigned* task_ctr;  // [1] next task of the bulk reduce's dynamic tail
   unsigned* scale_ctr; // [2] {next chunk, producers done} of the bulk scale's chunk queue
   unsigned* row_ctr;   // [2] {next row, CTAs done} of the register rows kernel's row queue
   unsigned* bp_ctr;    // [2] {next tile run, producers done} of the TMA backprop kernel
+  unsigned long long* arrivals;  // [1] fused kernel's grid barrier: CTA arrivals, never reset
   double* task_sums;   // [kMaxTasks] per-task sums of the dynamic tail
 };
 size_t workspace_bytes();
