@@ -11,10 +11,11 @@ CSRC    := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cpp)
 CHDR    := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/libnorm.h
 
 all: oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
-
+# Oracle: plain C, no contraction, no fast-math (threads only in the cpu_baseline timer
+# oracle_form_hoisted_mt, bit-identical to form 3); shares nothing with the CUDA path.
 # Oracle: plain C, no contraction, no fast-math, no threads; shares nothing with the CUDA path.
 oracle/liboracle.so: oracle/norm_oracle.c oracle/norm_oracle.h
-	$(CC) -std=c11 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
+	$(CC) -std=c11 -O2 -ffp-contract=off -fno-fast-math -pthread -fPIC -shared -o $@ $< -lm -lpthread
 
 gen/libnormgen.so: gen/gen_host.c gen/norm_gen.h
 	$(CC) -std=c11 -O2 -pthread -fPIC -shared -o $@ $< -lpthread

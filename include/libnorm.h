@@ -82,10 +82,15 @@ typedef enum {
   NORM_PATH_SMALL = 3     /* one CTA does everything (any n; intended for n <= 2^17)       */
 } norm_path_t;
 
+/* Options of every device entry point.  `index` and `path` carry norm_index_t /
+ * norm_path_t values but are declared int32_t: the width of a C enum is
+ * implementation-defined, and a fixed-width field keeps this struct's layout
+ * identical for every compiler and FFI (ctypes, Rust, ...).  Out-of-range values
+ * return NORM_ERR_INVALID_VALUE. */
 typedef struct {
   void* stream;         /* cudaStream_t to enqueue on; NULL = legacy default stream       */
-  int32_t index;        /* norm_index_t, default NORM_INDEX_LITERAL                        */
-  int32_t path;         /* norm_path_t, default NORM_PATH_AUTO                             */
+  int32_t index;        /* norm_index_t value, default NORM_INDEX_LITERAL                  */
+  int32_t path;         /* norm_path_t value, default NORM_PATH_AUTO                       */
   float* sum_out;       /* optional device ptr: receives s, the fp32 divisor used.
                            norm_rows: array of `rows` floats, one divisor per row          */
   double* sum_out_f64;  /* optional device ptr: receives S as accumulated (fp64).
@@ -95,12 +100,20 @@ typedef struct {
                            NULL = an internal cache keyed by (device, stream).  Calls that
                            may run concurrently must not share a workspace.                */
   size_t workspace_bytes;
-  void* ev_reduce_begin; /* optional cudaEvent_t recorded just before / after the reduce  */
-  void* ev_reduce_end;   /* kernel on `stream` (bench instrumentation); NULL = none        */
+  uint32_t flags;       /* NORM_FLAG_* bits; 0 = all checks                                */
+  uint32_t reserved;    /* must be 0                                                       */
 } norm_opts_t;
 
+/* The caller guarantees that every pointer it passes (in, out, sum_out,
+ * sum_out_f64) is device memory of the CURRENT device.  libnorm then skips its
+ * per-pointer cudaPointerGetAttributes checks (about 0.3-1 us of host time
+ * each; they exist to turn a host pointer into NORM_ERR_INVALID_VALUE instead of
+ * a sticky device fault).  For launch-bound callers (configs 1-2: n = 1024,
+ * 2^20 + 7).  A wrong pointer under this flag is a device fault. */
+#define NORM_FLAG_TRUSTED_PTRS 1u
+
 /* Designated defaults: literal index, AUTO path, default stream, no outputs. */
-#define NORM_OPTS_INIT {NULL, NORM_INDEX_LITERAL, NORM_PATH_AUTO, NULL, NULL, NULL, 0, NULL, NULL}
+#define NORM_OPTS_INIT {NULL, NORM_INDEX_LITERAL, NORM_PATH_AUTO, NULL, NULL, NULL, 0, 0u, 0u}
 
 /* ---------------------------------------------------------------- vector */
 
@@ -226,7 +239,9 @@ norm_status_t norm_bpnn_layerforward(const float* input, float* hidden, float* o
  * Pure host function (no CUDA call). */
 norm_status_t norm_coverage(int64_t n, int32_t index, int64_t* count, int64_t* prefix_len);
 
-/* Bytes of device workspace a call with (n, o) needs if the caller supplies one. */
+/* Bytes of device workspace a call with (n, o) needs if the caller supplies one
+ * (the per-CTA partials and queue counters of the reduce and
+ * scale kernels; independent of n today).  Host-only. */
 norm_status_t norm_workspace_bytes(int64_t n, const norm_opts_t* o, size_t* bytes);
 
 /* The path (norm_path_t) a call takes on the CURRENT device: `requested` if not
@@ -241,6 +256,12 @@ norm_status_t norm_choose_path(int64_t n, int64_t covered_prefix, int32_t reques
 norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t* bytes);
 
 /* --------------------------------------------------------- multi-GPU (NCCL) */
+/* The paper's method has one cross-thread dependency, the hoisted `sum`
+ * (PAPER.md:108, 117); sharded over W GPUs it becomes a local partial per rank
+ * plus an exchange of those 8-byte partials.  The paper itself scales only by
+ * MPI ranks under Horovod; the contiguous shards, the
+ * coverage-balanced plan and the "one NCCL all-reduce of a scalar" are the
+ * north_star's (BASELINE.json) and SURVEY.md §8(b)/(e)'s design, DESIGN.md §6. */
 
 /* Opaque: owns an ncclComm_t on the device current at init, plus device scratch
  * for the per-rank partial sums. One process per GPU. */
@@ -271,7 +292,8 @@ norm_status_t norm_comm_destroy(norm_comm_t* comm);
 typedef enum { NORM_COMM_ALLGATHER = 0, NORM_COMM_ALLREDUCE = 1 } norm_comm_mode_t;
 norm_status_t norm_comm_set_mode(norm_comm_t* comm, int32_t mode);
 
-/* Partition [0, n) over `world` ranks (pure host function; plan[world]).
+/* Partition [0, n) over `world` ranks (pure host function; plan[world]);
+ * SURVEY.md §8(e)(i)/(ii), north_star "partitioned ... by contiguous shards".
  * DENSE, or coverage_balanced == 0: one contiguous range per rank, boundaries
  * rounded to 8 elements.  LITERAL with coverage_balanced != 0 and a prefix
  * coverage [0, L): each rank gets a slice of [0, L) and a slice of [L, n), so
@@ -320,7 +342,12 @@ norm_status_t norm_shard_finish(float* out_local, const float* in_local, const n
  * fits); TWO_PASS (or a non-prefix local coverage) runs reduce -> scale.  Each
  * path is deterministic; their local partials differ only in summation order
  * (bit-identical whenever the fp64 accumulation is exact, e.g. grid-valued
- * inputs).  o->ev_reduce_* bracket the fused kernel when it runs. */
+ * inputs).
+ * Failure: if a call fails after this rank's publishing kernel was enqueued, the
+ * handle's epoch can no longer match its peers'; every later call on it returns
+ * NORM_ERR_CUDA ("peer handle broken") instead of waiting -- destroy and
+ * recreate the handles on every rank.  A call that fails before enqueueing
+ * anything leaves the handle usable. */
 typedef struct norm_peer norm_peer_t;
 norm_status_t norm_peer_create(norm_peer_t** peer, int32_t world, int32_t rank,
                                unsigned char handle[64]);
@@ -329,6 +356,15 @@ norm_status_t norm_peer_destroy(norm_peer_t* peer);
 norm_status_t norm_launch_sharded_peer(norm_peer_t* peer, float* out_local, const float* in_local,
                                        const norm_shard_t* mine, int64_t n_global,
                                        const norm_opts_t* o);
+
+/* -------------------------------------------------------- instrumentation */
+/* Not part of the operation: for timing the dominant kernel (bench.py's
+ * roofline).  begin / end are cudaEvent_t (or NULL).  Until called again, every
+ * vector or sharded call made on THIS host thread records `begin` on its stream
+ * immediately before its dominant kernel -- the reduce on two-pass paths, the
+ * one kernel on the small and fused paths -- and `end` immediately after it.
+ * (NULL, NULL) turns it off.  Ignored inside norm_graph_create. */
+norm_status_t norm_debug_set_events(void* begin, void* end);
 
 /* --------------------------------------------------------------- caches */
 /* Frees libnorm's internal per-(device, stream) caches: the ~161 KB workspaces and

@@ -42,6 +42,8 @@ def lib():
             getattr(L, f).restype = ctypes.c_double
         for f in ("oracle_form_thread", "oracle_form_block", "oracle_form_hoisted"):
             getattr(L, f).argtypes = [vp, vp, i64, ctypes.c_int, u64p]
+        L.oracle_form_hoisted_mt.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, u64p]
+        L.oracle_rows_sum_exact.argtypes = [vp, vp, i64, i64, i64]
         L.oracle_rows.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
         L.oracle_replay.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float]
         L.oracle_softmax_rows.argtypes = [vp, vp, i64, i64, i64, i64]
@@ -134,6 +136,32 @@ def form_block(inp, mode="literal", out=None):
 def form_hoisted(inp, mode="literal", out=None):
     """After parallel LICM: O(N) adds."""
     return _form("oracle_form_hoisted", inp, mode, out)
+
+
+def form_hoisted_mt(inp, mode="literal", threads=None, out=None):
+    """Form 3 on `threads` host threads (default: all cores): exact per-chunk
+    accumulators merged in chunk order, so bit-identical to form_hoisted.  Used to
+    time the oracle on the host's cores (bench.py cpu_baseline)."""
+    inp, pin = _f32(inp)
+    if out is None:
+        out = np.zeros_like(inp)
+    assert out.dtype == np.float32 and out.flags["C_CONTIGUOUS"] and out.size == inp.size
+    threads = (os.cpu_count() or 1) if threads is None else threads
+    adds = ctypes.c_uint64(0)
+    rc = lib().oracle_form_hoisted_mt(out.ctypes.data, pin, inp.size, _mode(mode), int(threads),
+                                      ctypes.byref(adds))
+    if rc:
+        raise ValueError("oracle_form_hoisted_mt rejected its arguments")
+    return out, adds.value
+
+
+def rows_sum_exact(x2d):
+    """Exact sum of every row of a 2-D float32 array, correctly rounded to fp64."""
+    x2d = np.ascontiguousarray(x2d, dtype=np.float32)
+    R, C = x2d.shape
+    S = np.zeros(R, dtype=np.float64)
+    assert lib().oracle_rows_sum_exact(S.ctypes.data, x2d.ctypes.data, R, C, C) == 0
+    return S
 
 
 def normalize(inp, mode="literal", out=None):

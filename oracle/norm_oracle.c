@@ -16,6 +16,7 @@
 #include "norm_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -229,6 +230,97 @@ int oracle_form_hoisted(float* out, const float* in, int64_t n, int mode, uint64
       if (tid < n) out[tid] = fig1_div(in[tid], val);
     }
   free(snapshot);
+  return 0;
+}
+
+/* Form 3 on T host threads, for timing the oracle on all of the host's cores
+ * (the cpu_baseline of bench.py).  Same arithmetic as
+ * oracle_form_hoisted: thread k accumulates the contiguous chunk
+ * [k n / T, (k+1) n / T) of `in` EXACTLY into its own superaccumulator; the T
+ * accumulators are merged in chunk order (integer limb addition: exact, so the
+ * merged value is the exact sum of all n terms whatever T is) and rounded once
+ * to fp64 -> val.  After a join (every load of the sum precedes every store,
+ * PAPER.md:598), thread k writes out[i] = in[i] / val for the covered i of its
+ * chunk (i in C(n) <=> some (b, t) of the launch has tid == i, PAPER.md:103,
+ * 109, 113).  Bit-identical to oracle_form_hoisted for every T (pinned). */
+typedef struct {
+  const float* in;
+  float* out;
+  int64_t lo, hi, n;
+  int mode;
+  double val;
+  acc_t acc;
+} mt_task_t;
+
+static void* mt_sum(void* arg) {
+  mt_task_t* k = (mt_task_t*)arg;
+  memset(&k->acc, 0, sizeof k->acc);
+  for (int64_t i = k->lo; i < k->hi; ++i) acc_add(&k->acc, k->in[i], 0);
+  acc_norm(&k->acc);
+  return NULL;
+}
+
+static void* mt_scale(void* arg) {
+  mt_task_t* k = (mt_task_t*)arg;
+  for (int64_t i = k->lo; i < k->hi; ++i)
+    if (oracle_is_covered(k->n, k->mode, i)) k->out[i] = fig1_div(k->in[i], k->val);
+  return NULL;
+}
+
+static int mt_run(mt_task_t* t, int T, void* (*fn)(void*)) {
+  pthread_t th[256];
+  int started = 0, rc = 0;
+  for (int k = 1; k < T; ++k) {
+    if (pthread_create(&th[k], NULL, fn, &t[k]) != 0) { rc = 3; break; }
+    started = k;
+  }
+  if (rc) { /* could not start every thread: run the rest here */
+    for (int k = started + 1; k < T; ++k) fn(&t[k]);
+    rc = 0;
+  }
+  fn(&t[0]);
+  for (int k = 1; k <= started; ++k) pthread_join(th[k], NULL);
+  return rc;
+}
+
+int oracle_form_hoisted_mt(float* out, const float* in, int64_t n, int mode, int threads,
+                           uint64_t* adds) {
+  if (n < 0 || (n > 0 && (!out || !in)) || threads < 1 || threads > 256) return 1;
+  if (n == 0) return 0;
+  mt_task_t* t = (mt_task_t*)calloc((size_t)threads, sizeof(mt_task_t));
+  if (!t) return 2;
+  for (int k = 0; k < threads; ++k) {
+    t[k].in = in;
+    t[k].out = out;
+    t[k].lo = n * k / threads;
+    t[k].hi = n * (k + 1) / threads;
+    t[k].n = n;
+    t[k].mode = mode;
+  }
+  mt_run(t, threads, mt_sum);
+  acc_t all;
+  memset(&all, 0, sizeof all);
+  for (int k = 0; k < threads; ++k) { /* chunk order; exact integer addition */
+    for (int j = 0; j < ACC_LIMBS; ++j) all.limb[j] += t[k].acc.limb[j];
+    all.nposinf += t[k].acc.nposinf;
+    all.nneginf += t[k].acc.nneginf;
+    all.nnan += t[k].acc.nnan;
+    all.nterms += t[k].acc.nterms;
+    all.nnegzero += t[k].acc.nnegzero;
+  }
+  if (adds) *adds += (uint64_t)n;
+  const double val = acc_result(&all);
+  for (int k = 0; k < threads; ++k) t[k].val = val;
+  mt_run(t, threads, mt_scale);
+  free(t);
+  return 0;
+}
+
+/* Exact per-row sums (the oracle's `sum` of each row, reading R10): S[r] = the
+ * exact sum of row r, correctly rounded to fp64. */
+int oracle_rows_sum_exact(double* S, const float* in, int64_t rows, int64_t cols, int64_t ld) {
+  if (rows < 0 || cols < 0 || ld < cols || (rows > 0 && (!S || (cols > 0 && !in)))) return 1;
+  for (int64_t r = 0; r < rows; ++r) S[r] = oracle_sum_exact(in + r * ld, cols);
   return 0;
 }
 

@@ -58,6 +58,14 @@ int oracle_form_thread(float* out, const float* in, int64_t n, int mode, uint64_
 int oracle_form_block(float* out, const float* in, int64_t n, int mode, uint64_t* adds);
 int oracle_form_hoisted(float* out, const float* in, int64_t n, int mode, uint64_t* adds);
 
+/* Form 3 on `threads` host threads (1..256): contiguous chunks accumulated
+ * exactly, merged in chunk order, one rounding -> bit-identical to
+ * oracle_form_hoisted.  For timing the oracle on all host cores (cpu_baseline). */
+int oracle_form_hoisted_mt(float* out, const float* in, int64_t n, int mode, int threads,
+                           uint64_t* adds);
+/* S[r] = exact sum of row r (in[r*ld + 0 .. cols)), correctly rounded to fp64. */
+int oracle_rows_sum_exact(double* S, const float* in, int64_t rows, int64_t cols, int64_t ld);
+
 /* Batched variant (reading R10): row r == oracle_form_hoisted on row r. */
 int oracle_rows(float* out, const float* in, int64_t rows, int64_t cols, int64_t ld_out,
                 int64_t ld_in, int mode);

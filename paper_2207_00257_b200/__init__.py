@@ -28,6 +28,7 @@ from ._lib import (  # noqa: F401
     norm_cache_release,
     norm_status_string,
     norm_last_error,
+    norm_debug_set_events,
     Comm,
     PeerComm,
     NormError,

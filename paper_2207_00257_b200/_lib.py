@@ -17,7 +17,10 @@ class NormOpts(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("index", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("sum_out", ctypes.c_void_p), ("sum_out_f64", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("ev_reduce_begin", ctypes.c_void_p), ("ev_reduce_end", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+FLAG_TRUSTED_PTRS = 1  # NORM_FLAG_TRUSTED_PTRS
 
 
 class NormShard(ctypes.Structure):
@@ -81,6 +84,8 @@ def lib():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        L.norm_debug_set_events.argtypes = [vp, vp]
+        L.norm_debug_set_events.restype = ctypes.c_int
         L.norm_cache_release.argtypes = []
         L.norm_cache_release.restype = ctypes.c_int
         L.norm_status_string.argtypes = [ctypes.c_int]
@@ -124,23 +129,54 @@ def _stream_handle(stream, device=None):
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _opts(index, path, stream, sum_out, sum_out_f64, workspace=None, events=None, device=None):
+def _opts(index, path, stream, sum_out, sum_out_f64, workspace=None, device=None, flags=0):
     o = NormOpts()
     o.stream = _stream_handle(stream, device)
     o.index = _enum(INDEX, index)
     o.path = _enum(PATH, path)
     o.sum_out = _ptr(sum_out)
     o.sum_out_f64 = _ptr(sum_out_f64)
+    o.flags = flags
     if workspace is not None:
         o.workspace = workspace.data_ptr()
         o.workspace_bytes = workspace.numel() * workspace.element_size()
-    if events is not None:
-        for ev in events:  # torch creates the CUDA event lazily, on first record
-            if not ev.cuda_event:
-                ev.record()
-        o.ev_reduce_begin = events[0].cuda_event
-        o.ev_reduce_end = events[1].cuda_event
     return o
+
+
+class _call:
+    """Context of one libnorm call from Python: makes the tensors' device current
+    (libnorm launches on the current device; a tensor on another GPU would be a
+    device fault) and, for the bench, arms norm_debug_set_events with a
+    (begin, end) torch.cuda.Event pair for the duration of the call."""
+    __slots__ = ("dev", "events", "prev")
+
+    def __init__(self, device, events=None):
+        self.dev = device
+        self.events = events
+        self.prev = None
+
+    def __enter__(self):
+        import torch
+        if self.dev is not None and self.dev.type == "cuda":
+            idx = self.dev.index if self.dev.index is not None else torch.cuda.current_device()
+            cur = torch.cuda.current_device()
+            if idx != cur:
+                self.prev = cur
+                torch.cuda.set_device(idx)
+        if self.events is not None:
+            for ev in self.events:  # torch creates the CUDA event lazily, on first record
+                if not ev.cuda_event:
+                    ev.record()
+            lib().norm_debug_set_events(self.events[0].cuda_event, self.events[1].cuda_event)
+        return self
+
+    def __exit__(self, *a):
+        if self.events is not None:
+            lib().norm_debug_set_events(None, None)
+        if self.prev is not None:
+            import torch
+            torch.cuda.set_device(self.prev)
+        return False
 
 
 def _check_f32(t, name, cuda=True):
@@ -152,19 +188,29 @@ def _check_f32(t, name, cuda=True):
 
 
 def normalize(out, inp, index="literal", path="auto", stream=None, sum_out=None,
-              sum_out_f64=None, workspace=None, events=None):
+              sum_out_f64=None, workspace=None, events=None, trusted=False):
     """out[C(n)] = inp[C(n)] / sum(inp) on the GPU (norm_launch_ex).  Returns out.
 
     out, inp: contiguous float32 CUDA tensors of equal numel (out may be inp).
     sum_out / sum_out_f64: optional 1-element float32 / float64 CUDA tensors.
-    events: optional (begin, end) torch.cuda.Event pair recorded around the reduce kernel.
+    events: optional (begin, end) torch.cuda.Event pair recorded around the call's
+    dominant kernel (norm_debug_set_events).
+    trusted: pass NORM_FLAG_TRUSTED_PTRS (skip libnorm's per-pointer checks; the
+    tensors are CUDA tensors of one device, checked here) -- for launch-bound sizes.
     """
     _check_f32(out, "out")
     _check_f32(inp, "inp")
     if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
         raise ValueError("out and inp must be contiguous with equal numel")
-    o = _opts(index, path, stream, sum_out, sum_out_f64, workspace, events, inp.device)
-    _check(lib().norm_launch_ex(out.data_ptr(), inp.data_ptr(), inp.numel(), ctypes.byref(o)))
+    flags = 0
+    if trusted:
+        for t in (out, sum_out, sum_out_f64):
+            if t is not None and (not t.is_cuda or t.device != inp.device):
+                raise ValueError("trusted=True needs every tensor on inp's CUDA device")
+        flags = FLAG_TRUSTED_PTRS
+    o = _opts(index, path, stream, sum_out, sum_out_f64, workspace, inp.device, flags)
+    with _call(inp.device, events):
+        _check(lib().norm_launch_ex(out.data_ptr(), inp.data_ptr(), inp.numel(), ctypes.byref(o)))
     return out
 
 
@@ -180,8 +226,9 @@ def normalize_form(out, inp, form="hoisted", index="literal", stream=None, sum_o
     if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
         raise ValueError("out and inp must be contiguous with equal numel")
     o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=inp.device)
-    _check(lib().norm_launch_form(out.data_ptr(), inp.data_ptr(), inp.numel(), _enum(FORM, form),
-                                  ctypes.byref(o)))
+    with _call(inp.device):
+        _check(lib().norm_launch_form(out.data_ptr(), inp.data_ptr(), inp.numel(), _enum(FORM, form),
+                                      ctypes.byref(o)))
     return out
 
 
@@ -197,8 +244,9 @@ def softmax_rows(out, inp, log=False, stream=None):
     if out.shape[1] > 1 and (out.stride(1) != 1 or inp.stride(1) != 1):
         raise ValueError("rows must have unit column stride")
     o = _opts("literal", "auto", stream, None, None, device=inp.device)
-    _check(lib().norm_softmax_rows(out.data_ptr(), inp.data_ptr(), inp.shape[0], inp.shape[1],
-                                   out.stride(0), inp.stride(0), 1 if log else 0, ctypes.byref(o)))
+    with _call(inp.device):
+        _check(lib().norm_softmax_rows(out.data_ptr(), inp.data_ptr(), inp.shape[0], inp.shape[1],
+                                       out.stride(0), inp.stride(0), 1 if log else 0, ctypes.byref(o)))
     return out
 
 
@@ -215,9 +263,10 @@ def nll_forward(logp, target, weight=None, reduction="mean", ignore_index=-100, 
     loss = torch.empty(N if red == 0 else 1, dtype=torch.float32, device=logp.device)
     tw = torch.empty(1, dtype=torch.float32, device=logp.device)
     o = _opts("literal", "auto", stream, None, None, device=logp.device)
-    _check(lib().norm_nll_forward(loss.data_ptr(), tw.data_ptr(), logp.data_ptr(), target.data_ptr(),
-                                  _ptr(weight), N, C, logp.stride(0), red, ignore_index,
-                                  ctypes.byref(o)))
+    with _call(logp.device):
+        _check(lib().norm_nll_forward(loss.data_ptr(), tw.data_ptr(), logp.data_ptr(), target.data_ptr(),
+                                      _ptr(weight), N, C, logp.stride(0), red, ignore_index,
+                                      ctypes.byref(o)))
     return (loss if red == 0 else loss[0]), tw
 
 
@@ -229,9 +278,10 @@ def nll_backward(grad_out, logp_shape, target, total_weight, weight=None, reduct
     if grad is None:
         grad = torch.empty((N, C), dtype=torch.float32, device=target.device)
     o = _opts("literal", "auto", stream, None, None, device=target.device)
-    _check(lib().norm_nll_backward(grad.data_ptr(), grad_out.data_ptr(), target.data_ptr(),
-                                   _ptr(weight), _ptr(total_weight), N, C, grad.stride(0),
-                                   _enum(REDUCTION, reduction), ignore_index, ctypes.byref(o)))
+    with _call(target.device):
+        _check(lib().norm_nll_backward(grad.data_ptr(), grad_out.data_ptr(), target.data_ptr(),
+                                       _ptr(weight), _ptr(total_weight), N, C, grad.stride(0),
+                                       _enum(REDUCTION, reduction), ignore_index, ctypes.byref(o)))
     return grad
 
 
@@ -250,8 +300,9 @@ def bpnn_layerforward(input_units, hidden, output, variant="register", stream=No
     if hidden.numel() != (n_in + 1) * (hid + 1) or output.numel() < n_in:
         raise ValueError("shapes: input [in+1], hidden [in+1, hid+1], output [in]")
     o = _opts("literal", "auto", stream, None, None, device=hidden.device)
-    _check(lib().norm_bpnn_layerforward(input_units.data_ptr(), hidden.data_ptr(), output.data_ptr(),
-                                        n_in, hid, _enum(BP_VARIANT, variant), ctypes.byref(o)))
+    with _call(hidden.device):
+        _check(lib().norm_bpnn_layerforward(input_units.data_ptr(), hidden.data_ptr(), output.data_ptr(),
+                                            n_in, hid, _enum(BP_VARIANT, variant), ctypes.byref(o)))
     return hidden, output
 
 
@@ -267,13 +318,15 @@ class NormGraph:
         self._keep = (out, inp, sum_out, sum_out_f64)  # the graph holds raw pointers
         o = _opts(index, path, None, sum_out, sum_out_f64, device=inp.device)
         h = ctypes.c_void_p()
-        _check(lib().norm_graph_create(ctypes.byref(h), out.data_ptr(), inp.data_ptr(), inp.numel(),
-                                       ctypes.byref(o)))
+        with _call(inp.device):
+            _check(lib().norm_graph_create(ctypes.byref(h), out.data_ptr(), inp.data_ptr(), inp.numel(),
+                                           ctypes.byref(o)))
         self._h = h
         self._device = inp.device
 
     def launch(self, stream=None):
-        _check(lib().norm_graph_launch(self._h, _stream_handle(stream, self._device)))
+        with _call(self._device):
+            _check(lib().norm_graph_launch(self._h, _stream_handle(stream, self._device)))
 
     def destroy(self):
         if self._h:
@@ -297,8 +350,9 @@ def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out
         raise ValueError("rows must have unit column stride")
     rows, cols = inp.shape
     o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=inp.device)
-    _check(lib().norm_rows(out.data_ptr(), inp.data_ptr(), rows, cols, out.stride(0),
-                           inp.stride(0), ctypes.byref(o)))
+    with _call(inp.device):
+        _check(lib().norm_rows(out.data_ptr(), inp.data_ptr(), rows, cols, out.stride(0),
+                               inp.stride(0), ctypes.byref(o)))
     return out
 
 
@@ -380,15 +434,17 @@ def normalize_sharded_via(out_local, in_local, ranges, n_global, all_gather, ind
     if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
         raise ValueError("local buffers must hold exactly the shard's elements")
     part = torch.empty(1, dtype=torch.float64, device=in_local.device)
-    o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
-    _check(lib().norm_shard_partial(part.data_ptr(), in_local.data_ptr(), in_local.numel(),
-                                    ctypes.byref(o)))
+    o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=in_local.device)
+    with _call(in_local.device, events):
+        _check(lib().norm_shard_partial(part.data_ptr(), in_local.data_ptr(), in_local.numel(),
+                                        ctypes.byref(o)))
     parts = all_gather(part)
     if parts.dtype != torch.float64 or not parts.is_cuda or not parts.is_contiguous():
         raise ValueError("all_gather must return a contiguous float64 CUDA tensor")
     shard = _shard_struct(ranges)
-    _check(lib().norm_shard_finish(out_local.data_ptr(), in_local.data_ptr(), ctypes.byref(shard),
-                                   n_global, parts.data_ptr(), parts.numel(), ctypes.byref(o)))
+    with _call(in_local.device):
+        _check(lib().norm_shard_finish(out_local.data_ptr(), in_local.data_ptr(), ctypes.byref(shard),
+                                       n_global, parts.data_ptr(), parts.numel(), ctypes.byref(o)))
     return out_local
 
 
@@ -421,9 +477,10 @@ class Comm:
         shard = _shard_struct(ranges)
         if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
             raise ValueError("local buffers must hold exactly the shard's elements")
-        o = _opts(index, "auto", stream, sum_out, sum_out_f64, events=events, device=in_local.device)
-        _check(lib().norm_launch_sharded(self._h, out_local.data_ptr(), in_local.data_ptr(),
-                                         ctypes.byref(shard), n_global, ctypes.byref(o)))
+        o = _opts(index, "auto", stream, sum_out, sum_out_f64, device=in_local.device)
+        with _call(in_local.device, events):
+            _check(lib().norm_launch_sharded(self._h, out_local.data_ptr(), in_local.data_ptr(),
+                                             ctypes.byref(shard), n_global, ctypes.byref(o)))
         return out_local
 
     def destroy(self):
@@ -475,9 +532,10 @@ class PeerComm:
         if in_local.numel() != sum(ln for _, ln in ranges) or out_local.numel() != in_local.numel():
             raise ValueError("local buffers must hold exactly the shard's elements")
         shard = _shard_struct(ranges)
-        o = _opts(index, path, stream, sum_out, sum_out_f64, events=events, device=in_local.device)
-        _check(lib().norm_launch_sharded_peer(self._h, out_local.data_ptr(), in_local.data_ptr(),
-                                              ctypes.byref(shard), n_global, ctypes.byref(o)))
+        o = _opts(index, path, stream, sum_out, sum_out_f64, device=in_local.device)
+        with _call(in_local.device, events):
+            _check(lib().norm_launch_sharded_peer(self._h, out_local.data_ptr(), in_local.data_ptr(),
+                                                  ctypes.byref(shard), n_global, ctypes.byref(o)))
         return out_local
 
     def destroy(self):
@@ -528,3 +586,15 @@ norm_plan_shards = plan_shards
 norm_cache_release = cache_release
 norm_status_string = status_string
 norm_last_error = last_error
+
+
+def norm_debug_set_events(begin=None, end=None):
+    """norm_debug_set_events: (begin, end) torch.cuda.Event pair recorded around the
+    dominant kernel of every later call on this thread; (None, None) turns it off."""
+    if begin is None or end is None:
+        _check(lib().norm_debug_set_events(None, None))
+        return
+    for ev in (begin, end):
+        if not ev.cuda_event:
+            ev.record()
+    _check(lib().norm_debug_set_events(begin.cuda_event, end.cuda_event))

@@ -250,19 +250,21 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
   if (!o) o = &kDef;
   if (!c) return fail(NORM_ERR_INVALID_VALUE, "comm is NULL");
   int64_t local = 0;
-  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  norm_status_t s = check_opts(o);
   if (s != NORM_OK) return s;
+  if ((s = check_shard(out_local, in_local, mine, n_global, o, &local)) != NORM_OK) return s;
   DeviceInfo d;
-  std::string err;
-  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if ((s = check_device(&d)) != NORM_OK) return s;
   if (d.device != c->device) return fail(NORM_ERR_INVALID_VALUE, "current device != comm device");
+  if (local > 0 && (s = check_io_ptrs(out_local, in_local, o, d)) != NORM_OK) return s;
+  if (local == 0 && (s = check_out_ptrs(o, d)) != NORM_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Workspace ws = workspace_carve(c->ws);
   // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
-  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  ev_begin(st);
   cudaError_t e = launch_reduce(in_local, local, ws, c->send, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  ev_end(st);
   // 2. exchange: W x 8 bytes over NVLink
   if (c->mode == NORM_COMM_ALLREDUCE) {  // NCCL's own summation order; one partial back
     ncclResult_t r = ncclAllReduce(c->send, c->recv, 1, ncclFloat64, ncclSum, c->nccl, st);
@@ -283,17 +285,24 @@ NORM_API norm_status_t norm_shard_partial(double* partial, const float* in_local
     return fail(NORM_ERR_INVALID_VALUE, "bad partial arguments");
   if (reinterpret_cast<uintptr_t>(in_local) & 3u)
     return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  norm_status_t s = check_opts(o);
+  if (s != NORM_OK) return s;
   DeviceInfo d;
-  std::string err;
-  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  // the partial is written by the kernel: it must be device memory of this device
+  norm_opts_t po = NORM_OPTS_INIT;
+  po.flags = o->flags;
+  po.sum_out_f64 = partial;
+  if ((s = check_out_ptrs(&po, d)) != NORM_OK) return s;
+  if (n_local > 0 && (s = check_io_ptrs(in_local, in_local, o, d)) != NORM_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Workspace ws;
-  norm_status_t s = get_workspace(o, d.device, st, &ws);
+  s = get_workspace(o, d.device, st, &ws);
   if (s != NORM_OK) return s;
-  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  ev_begin(st);
   cudaError_t e = launch_reduce(in_local, n_local, ws, partial, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  ev_end(st);
   return NORM_OK;
 }
 
@@ -305,11 +314,13 @@ NORM_API norm_status_t norm_shard_finish(float* out_local, const float* in_local
   if (!o) o = &kDef;
   if (!partials || world < 1) return fail(NORM_ERR_INVALID_VALUE, "bad partials");
   int64_t local = 0;
-  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  norm_status_t s = check_opts(o);
   if (s != NORM_OK) return s;
+  if ((s = check_shard(out_local, in_local, mine, n_global, o, &local)) != NORM_OK) return s;
   DeviceInfo d;
-  std::string err;
-  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if ((s = check_device(&d)) != NORM_OK) return s;
+  if (local > 0 && (s = check_io_ptrs(out_local, in_local, o, d)) != NORM_OK) return s;
+  if (local == 0 && (s = check_out_ptrs(o, d)) != NORM_OK) return s;
   Workspace ws;
   s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws);
   if (s != NORM_OK) return s;
@@ -329,6 +340,7 @@ struct norm_peer {
   double** peer_dev = nullptr;   // device array: mailbox of rank r as mapped here
   std::vector<void*> opened;     // IPC mappings to close
   unsigned long long epoch = 0;
+  bool broken = false;           // a call failed after publishing: epochs out of step
   void* ws = nullptr;            // reduce workspace
 };
 
@@ -405,15 +417,22 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
   static const norm_opts_t kDef = NORM_OPTS_INIT;
   if (!o) o = &kDef;
   if (!p) return fail(NORM_ERR_INVALID_VALUE, "peer is NULL");
+  if (p->broken)
+    return fail(NORM_ERR_CUDA, "peer handle broken by an earlier failed call: destroy and recreate it on every rank");
   int64_t local = 0;
-  norm_status_t s = check_shard(out_local, in_local, mine, n_global, o, &local);
+  norm_status_t s = check_opts(o);
   if (s != NORM_OK) return s;
+  if ((s = check_shard(out_local, in_local, mine, n_global, o, &local)) != NORM_OK) return s;
   DeviceInfo d;
-  std::string err;
-  if (!device_info(&d, &err)) return fail(NORM_ERR_CUDA, err);
+  if ((s = check_device(&d)) != NORM_OK) return s;
   if (d.device != p->device) return fail(NORM_ERR_INVALID_VALUE, "current device != peer device");
+  if (local > 0 && (s = check_io_ptrs(out_local, in_local, o, d)) != NORM_OK) return s;
+  if (local == 0 && (s = check_out_ptrs(o, d)) != NORM_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
-  const unsigned long long epoch = ++p->epoch;
+  // The epoch is committed only once this rank's kernels are enqueued; a failure
+  // after the publishing kernel was enqueued leaves the peers one epoch ahead of
+  // us, so the handle is marked broken instead (include/libnorm.h).
+  const unsigned long long epoch = p->epoch + 1;
   Workspace ws = workspace_carve(p->ws);
   const PeerPost post{p->peer_dev, p->rank, p->world, epoch};
   // One fused kernel per rank (reduce, grid barrier, publish + mailbox wait,
@@ -431,16 +450,23 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
     lc.n = local;
     lc.L = lc.count = Lloc;
     lc.G = (local + 31) / 32;
-    if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+    ev_begin(st);
     cudaError_t e = launch_fused(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post,
                                  p->mail);
-    if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");
-    if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");  // nothing enqueued
+    ev_end(st);
+    p->epoch = epoch;
     return NORM_OK;
   }
-  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  ev_begin(st);
   cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st, post);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
-  return shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, ws, epoch);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");  // nothing enqueued
+  ev_end(st);
+  s = shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, ws, epoch);
+  if (s != NORM_OK) {
+    p->broken = true;  // the reduce has published this epoch; our scale did not consume it
+    return s;
+  }
+  p->epoch = epoch;
+  return NORM_OK;
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -28,6 +29,19 @@ norm_status_t fail(norm_status_t st, const std::string& s) {
 norm_status_t cuda_fail(cudaError_t e, const char* what) {
   set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
   return NORM_ERR_CUDA;
+}
+
+// ------------------------------------------------ instrumentation (bench only)
+// norm_debug_set_events: events recorded around the dominant kernel of every
+// call on this host thread; suppressed while norm_graph_create captures.
+static thread_local cudaEvent_t g_ev_begin = nullptr, g_ev_end = nullptr;
+static thread_local bool g_capturing = false;
+
+void ev_begin(cudaStream_t st) {
+  if (g_ev_begin && !g_capturing) cudaEventRecord(g_ev_begin, st);
+}
+void ev_end(cudaStream_t st) {
+  if (g_ev_end && !g_capturing) cudaEventRecord(g_ev_end, st);
 }
 
 // ---------------------------------------------------------------- coverage
@@ -114,7 +128,7 @@ bool device_info(DeviceInfo* out, std::string* err) {
   return true;
 }
 
-static norm_status_t check_device(DeviceInfo* d) {
+norm_status_t check_device(DeviceInfo* d) {
   std::string err;
   if (!device_info(d, &err)) return fail(NORM_ERR_CUDA, err);
   if (d->cc_major != 10 || d->cc_minor != 0)
@@ -153,8 +167,24 @@ Workspace workspace_carve(void* base) {
 // until norm_cache_release().
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, cudaStream_t>, void*> g_ws_cache;
+// Bumped by norm_cache_release; a thread's one-entry memo of its last (device,
+// stream) -> workspace lookup is valid only for the generation it was made in
+// (saves the mutex + map lookup on back-to-back calls: configs 1-2 are host-bound).
+static std::atomic<unsigned long long> g_ws_gen{1};
+struct WsMemo {
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  void* p = nullptr;
+  unsigned long long gen = 0;
+};
+static thread_local WsMemo g_ws_memo;
 
 static norm_status_t internal_workspace(int dev, cudaStream_t st, Workspace* ws) {
+  WsMemo& m = g_ws_memo;
+  if (m.p && m.dev == dev && m.st == st && m.gen == g_ws_gen.load(std::memory_order_acquire)) {
+    *ws = workspace_carve(m.p);
+    return NORM_OK;
+  }
   std::mutex& mu = g_ws_mu;
   auto& cache = g_ws_cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -173,6 +203,10 @@ static norm_status_t internal_workspace(int dev, cudaStream_t st, Workspace* ws)
     it = cache.emplace(key, p).first;
   }
   *ws = workspace_carve(it->second);
+  m.dev = dev;
+  m.st = st;
+  m.p = it->second;
+  m.gen = g_ws_gen.load(std::memory_order_acquire);
   return NORM_OK;
 }
 
@@ -191,11 +225,13 @@ norm_status_t get_workspace(const norm_opts_t* o, int dev, cudaStream_t st, Work
 // ------------------------------------------------------------ validation
 static bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
-static norm_status_t check_opts(const norm_opts_t* o) {
+norm_status_t check_opts(const norm_opts_t* o) {
   if (o->index != NORM_INDEX_LITERAL && o->index != NORM_INDEX_DENSE)
     return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
   if (o->path < NORM_PATH_AUTO || o->path > NORM_PATH_SMALL)
     return fail(NORM_ERR_INVALID_VALUE, "bad path");
+  if ((o->flags & ~NORM_FLAG_TRUSTED_PTRS) != 0u || o->reserved != 0u)
+    return fail(NORM_ERR_INVALID_VALUE, "unknown flags or nonzero reserved field");
   return NORM_OK;
 }
 
@@ -206,7 +242,13 @@ static bool partial_overlap(const void* a, size_t na, const void* b, size_t nb) 
   return x < y + nb && y < x + na;
 }
 
-static norm_status_t check_device_ptr(const void* p, const char* name) {
+// A pointer the kernels dereference must be device (or managed) memory of the
+// current device: a host pointer, or device memory of another GPU launched on
+// from this one, is a sticky device fault, so it is rejected up front.  Skipped
+// under NORM_FLAG_TRUSTED_PTRS (the caller vouches; launch-bound callers).
+static norm_status_t check_device_ptr(const void* p, const char* name, const DeviceInfo& d,
+                                      const norm_opts_t* o) {
+  if (o && (o->flags & NORM_FLAG_TRUSTED_PTRS)) return NORM_OK;
   cudaPointerAttributes at;
   cudaError_t e = cudaPointerGetAttributes(&at, p);
   if (e != cudaSuccess) {
@@ -216,16 +258,26 @@ static norm_status_t check_device_ptr(const void* p, const char* name) {
   if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
     return fail(NORM_ERR_INVALID_VALUE, std::string(name) +
                                             " is not device memory (use norm_launch_host for host buffers)");
+  if (at.type == cudaMemoryTypeDevice && at.device != d.device)
+    return fail(NORM_ERR_INVALID_VALUE, std::string(name) + " lives on device " +
+                                            std::to_string(at.device) + " but the current device is " +
+                                            std::to_string(d.device) + " (cudaSetDevice first)");
   return NORM_OK;
 }
 
-// sum_out / sum_out_f64 are written by the kernels: a host pointer there would be a
-// device fault (sticky), so it is rejected up front.
-static norm_status_t check_out_ptrs(const norm_opts_t* o) {
+norm_status_t check_out_ptrs(const norm_opts_t* o, const DeviceInfo& d) {
   norm_status_t s;
-  if (o->sum_out && (s = check_device_ptr(o->sum_out, "sum_out")) != NORM_OK) return s;
-  if (o->sum_out_f64 && (s = check_device_ptr(o->sum_out_f64, "sum_out_f64")) != NORM_OK) return s;
+  if (o->sum_out && (s = check_device_ptr(o->sum_out, "sum_out", d, o)) != NORM_OK) return s;
+  if (o->sum_out_f64 && (s = check_device_ptr(o->sum_out_f64, "sum_out_f64", d, o)) != NORM_OK) return s;
   return NORM_OK;
+}
+
+norm_status_t check_io_ptrs(const float* out, const float* in, const norm_opts_t* o,
+                            const DeviceInfo& d) {
+  norm_status_t s;
+  if ((s = check_device_ptr(in, "in", d, o)) != NORM_OK) return s;
+  if (out != in && (s = check_device_ptr(out, "out", d, o)) != NORM_OK) return s;
+  return check_out_ptrs(o, d);
 }
 
 static norm_status_t check_vector_args(float* out, const float* in, int64_t n) {
@@ -276,20 +328,26 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
   if (path == NORM_PATH_FUSED && cov.kind != COV_PREFIX) path = NORM_PATH_SMALL;
   cudaError_t e;
   if (path == NORM_PATH_SMALL) {
+    ev_begin(st);
     e = launch_small(out, in, cov, o->sum_out, o->sum_out_f64, st);
-    return e == cudaSuccess ? NORM_OK : cuda_fail(e, "small_kernel launch");
+    if (e != cudaSuccess) return cuda_fail(e, "small_kernel launch");
+    ev_end(st);
+    return NORM_OK;
   }
   Workspace ws;
   norm_status_t s = get_workspace(o, d.device, st, &ws);
   if (s != NORM_OK) return s;
   if (path == NORM_PATH_FUSED) {
+    ev_begin(st);
     e = launch_fused(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
-    return e == cudaSuccess ? NORM_OK : cuda_fail(e, "fused_kernel cooperative launch");
+    if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");
+    ev_end(st);
+    return NORM_OK;
   }
-  if (o->ev_reduce_begin) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_begin), st);
+  ev_begin(st);
   e = launch_reduce(in, cov.n, ws, ws.S, d, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  if (o->ev_reduce_end) cudaEventRecord(static_cast<cudaEvent_t>(o->ev_reduce_end), st);
+  ev_end(st);
   if (cov.kind == COV_PREFIX)
     e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st, 0, ws.scale_ctr);
   else
@@ -468,9 +526,7 @@ NORM_API norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, co
   if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
-  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
-  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
-  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  if ((s = check_io_ptrs(out, in, o, d)) != NORM_OK) return s;
   return launch_vector(out, in, cov, o, d);
 }
 
@@ -508,9 +564,7 @@ NORM_API norm_status_t norm_graph_create(norm_graph_t** out_g, float* out, const
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
   if (n > 0) {
-    if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
-    if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
-    if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+    if ((s = check_io_ptrs(out, in, o, d)) != NORM_OK) return s;
   }
   norm_graph* g = new norm_graph();
   g->device = d.device;
@@ -531,10 +585,12 @@ NORM_API norm_status_t norm_graph_create(norm_graph_t** out_g, float* out, const
   oc.stream = g->cap;
   oc.workspace = g->ws;
   oc.workspace_bytes = workspace_bytes();
-  oc.ev_reduce_begin = oc.ev_reduce_end = nullptr;
+  oc.flags |= NORM_FLAG_TRUSTED_PTRS;  // checked above
   if ((e = cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaStreamBeginCapture"));
+  g_capturing = true;
   s = n > 0 ? launch_vector(out, in, cov, &oc, d) : NORM_OK;
+  g_capturing = false;
   cudaGraph_t graph = nullptr;
   e = cudaStreamEndCapture(g->cap, &graph);
   if (s != NORM_OK) {
@@ -583,9 +639,7 @@ NORM_API norm_status_t norm_launch_form(float* out, const float* in, int64_t n, 
   if (n > (1ll << 24)) return fail(NORM_ERR_UNSUPPORTED, "un-hoisted forms are O(N^2): n <= 2^24");
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
-  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
-  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
-  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  if ((s = check_io_ptrs(out, in, o, d)) != NORM_OK) return s;
   cudaError_t e = launch_unhoisted(out, in, n, o->index, form, o->sum_out, o->sum_out_f64,
                                    static_cast<cudaStream_t>(o->stream));
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "unhoisted kernel launch");
@@ -602,7 +656,7 @@ NORM_API norm_status_t norm_launch_host(float* out_host, const float* in_host, i
   if ((s = check_literal_grid(cov, o->index)) != NORM_OK) return s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
-  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  if ((s = check_out_ptrs(o, d)) != NORM_OK) return s;
   return launch_host(out_host, in_host, cov, o, d);
 }
 
@@ -624,9 +678,7 @@ NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int6
   const Coverage rc = coverage_of(cols, o->index);
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
-  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
-  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
-  if ((s = check_out_ptrs(o)) != NORM_OK) return s;
+  if ((s = check_io_ptrs(out, in, o, d)) != NORM_OK) return s;
   Workspace ws;
   if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_rows(out, in, rows, cols, ld_out, ld_in, rc, o->sum_out, o->sum_out_f64, d,
@@ -651,8 +703,8 @@ NORM_API norm_status_t norm_softmax_rows(float* out, const float* in, int64_t ro
   norm_status_t s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
-  if ((s = check_device_ptr(in, "in")) != NORM_OK) return s;
-  if ((s = check_device_ptr(out, "out")) != NORM_OK) return s;
+  if ((s = check_device_ptr(in, "in", d, o)) != NORM_OK) return s;
+  if (out != in && (s = check_device_ptr(out, "out", d, o)) != NORM_OK) return s;
   Workspace ws;
   if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_softmax_rows(out, in, rows, cols, ld_out, ld_in, kind == NORM_LOG_SOFTMAX, d,
@@ -752,11 +804,18 @@ NORM_API norm_status_t norm_algorithmic_bytes(int64_t n, int32_t index, int64_t*
   return NORM_OK;
 }
 
+NORM_API norm_status_t norm_debug_set_events(void* begin, void* end) {
+  g_ev_begin = static_cast<cudaEvent_t>(begin);
+  g_ev_end = static_cast<cudaEvent_t>(end);
+  return NORM_OK;
+}
+
 NORM_API norm_status_t norm_cache_release(void) {
   int cur = -1;
   cudaGetDevice(&cur);
   {
     std::lock_guard<std::mutex> lk(g_ws_mu);
+    g_ws_gen.fetch_add(1, std::memory_order_acq_rel);  // invalidates every thread's memo
     for (auto& kv : g_ws_cache) {
       cudaSetDevice(kv.first.first);
       cudaDeviceSynchronize();

@@ -146,6 +146,18 @@ cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_
 // or not a prefix (libnorm.cpp; also used per rank by the sharded peer path).
 int auto_path(int64_t n, int64_t L, bool prefix, const DeviceInfo& d);
 
+// Argument checks shared by the C ABI entry points (libnorm.cpp).
+norm_status_t check_device(DeviceInfo* d);  // current device, must be sm_100
+norm_status_t check_opts(const norm_opts_t* o);
+norm_status_t check_out_ptrs(const norm_opts_t* o, const DeviceInfo& d);  // sum_out, sum_out_f64
+norm_status_t check_io_ptrs(const float* out, const float* in, const norm_opts_t* o,
+                            const DeviceInfo& d);  // + in, out
+
+// norm_debug_set_events instrumentation: record this thread's begin / end event
+// (if set, and not while a graph is being captured) on `st`.
+void ev_begin(cudaStream_t st);
+void ev_end(cudaStream_t st);
+
 // thread-local error detail
 void set_error(const std::string& s);
 norm_status_t fail(norm_status_t st, const std::string& s);

@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(SM_THREADS, sm_ctas_per_sm(MAXV))
     r = rn;
     rn = rnn;
   }
+  if (ctr && threadIdx.x == 0) __threadfence();  // claims on ctr[0] precede the count
   if (ctr && threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // all CTAs done claiming
+    __threadfence();  // every other CTA's claims are visible before the reset
     ctr[0] = 0u;
     ctr[1] = 0u;
   }

@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
     r = rn;
     rn = rnn;
   }
+  if (ctr && threadIdx.x == 0) __threadfence();  // claims on ctr[0] precede the count
   if (ctr && threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // all CTAs done claiming
+    __threadfence();  // every other CTA's claims are visible before the reset
     ctr[0] = 0u;
     ctr[1] = 0u;
   }
@@ -185,7 +187,9 @@ __global__ void __launch_bounds__(32 * (1 + RB_MAX_WARPS), 1)
           next = rs + (int64_t)atomicAdd(ctr, 1u);
           issue(r);
         }
+        __threadfence();  // this CTA's claims on ctr[0] precede its count on ctr[1]
         if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every producer has claimed its last row
+          __threadfence();  // every other CTA's claims are visible before the reset
           ctr[0] = 0u;
           ctr[1] = 0u;
         }

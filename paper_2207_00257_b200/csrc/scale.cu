@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
           ++r.issued;
           r.advance();
         }
+        __threadfence();  // this CTA's claims on ctr[0] precede its count on ctr[1]
         if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every producer has claimed its last chunk
+          __threadfence();  // every other CTA's claims are visible before the reset
           ctr[0] = 0u;
           ctr[1] = 0u;
         }

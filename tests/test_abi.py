@@ -101,6 +101,12 @@ def test_invalid_arguments_rejected_before_cuda():
     assert lib.norm_launch_ex(vp(4096), vp(8192), 1, ctypes.byref(o)) == E("NORM_ERR_INVALID_VALUE")
     o.index, o.path = 0, 9
     assert lib.norm_launch_ex(vp(4096), vp(8192), 1, ctypes.byref(o)) == E("NORM_ERR_INVALID_VALUE")
+    o.path = 0
+    o.flags = 2  # unknown flag bit
+    assert lib.norm_launch_ex(vp(4096), vp(8192), 1, ctypes.byref(o)) == E("NORM_ERR_INVALID_VALUE")
+    o.flags, o.reserved = 0, 1
+    assert lib.norm_launch_ex(vp(4096), vp(8192), 1, ctypes.byref(o)) == E("NORM_ERR_INVALID_VALUE")
+    assert lib.norm_shard_partial(vp(4096), vp(8192), 8, ctypes.byref(o)) == E("NORM_ERR_INVALID_VALUE")
     # literal grid beyond gridDim.x: G = ceil(n/32) > 2^31 - 1
     big = 32 * (2**31 - 1) + 1
     assert lib.norm_launch(vp(1 << 44), vp(1 << 46), big) == E("NORM_ERR_UNSUPPORTED")
@@ -149,3 +155,34 @@ def test_binding_has_c_names():
         if name not in skip:
             assert hasattr(L, name), name
     assert L.norm_coverage(2**32) == (134218720, 134218720)
+
+
+def test_opts_layout_matches_header():
+    """norm_opts_t as ctypes sees it == the C struct (offsets of every field)."""
+    import subprocess
+    import tempfile
+    src = r"""
+#include <stddef.h>
+#include <stdio.h>
+#include "libnorm.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(norm_opts_t),
+         offsetof(norm_opts_t, stream), offsetof(norm_opts_t, index), offsetof(norm_opts_t, path),
+         offsetof(norm_opts_t, sum_out), offsetof(norm_opts_t, sum_out_f64),
+         offsetof(norm_opts_t, workspace), offsetof(norm_opts_t, workspace_bytes),
+         offsetof(norm_opts_t, flags), offsetof(norm_opts_t, reserved));
+  return 0;
+}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "o.c")
+        with open(c, "w") as f:
+            f.write(src)
+        exe = os.path.join(d, "o")
+        subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    O = L._lib.NormOpts
+    want = [ctypes.sizeof(O)] + [getattr(O, f).offset for f in
+                                 ("stream", "index", "path", "sum_out", "sum_out_f64", "workspace",
+                                  "workspace_bytes", "flags", "reserved")]
+    assert got == want

@@ -62,7 +62,12 @@ def check(x, out, s, mode, dist_kind, before=None):
     cov = oracle.covered_mask(n, mode)
     r, o = ref[cov].astype(np.float64), out[cov].astype(np.float64)
     nz = r != 0
-    if dist_kind != 3:  # signed: ill-conditioned quotient, replay above is the check
+    # Signed inputs (D3): the quotient of a cancelling sum is ill-conditioned, so
+    # the per-element 1e-5 check is skipped.  By SURVEY readings P19/P20 the
+    # check is still complete: s is bounded by 1e-6 of the exact sum of |x|
+    # above, and given s every output is unique -- the bitwise replay against
+    # the oracle's binary32 RN division above pins it.
+    if dist_kind != 3:
         assert np.all(np.abs(o[nz] - r[nz]) <= 1e-5 * np.abs(r[nz]))
         assert np.all(o[~nz] == 0)
 
@@ -198,6 +203,16 @@ def test_large_sampled_2_28():
 
 @pytest.mark.parametrize("mode", ["literal", "dense"])
 def test_rows_parity(mode):
+    """Every row of every shape, including the full 65536 x 4096 config and the
+    (300, 2048) padded shape that exercises the register kernel's row queue:
+    each row's divisor s_r against the oracle's exact sum of THAT row (so a row
+    scaled by another row's divisor fails), every covered output within 1e-5 of
+    the oracle's rows form, the whole matrix replayed bitwise with its own s_r,
+    and every uncovered / padding element still holding the sentinel.  Signed
+    rows (D3) bound s_r by 1e-6 of the row's exact sum of |x| and skip the
+    per-element relative check (readings P19/P20 of the survey: the quotient of
+    a cancelling sum is ill-conditioned; the bitwise replay against the oracle's
+    RN32 division plus the Σ|x|-scaled bound on s_r is the complete check)."""
     # kernel coverage: 65536x4096 / 5x10000 / 1x8192 literal -> TMA warp-per-row kernel
     # (9x512 literal: residue coverage there); dense and other shapes -> register-
     # resident CTA-per-row kernel; 4099 / 703 / 72 -> generic kernel
@@ -211,18 +226,32 @@ def test_rows_parity(mode):
         inp = to_dev(x)
         out = to_dev(sentinel(R * ld).reshape(R, ld))
         s = torch.zeros(R, device="cuda")
-        L.normalize_rows(out[:, :C], inp[:, :C], index=mode, sum_out=s)
+        s64 = torch.zeros(R, dtype=torch.float64, device="cuda")
+        L.normalize_rows(out[:, :C], inp[:, :C], index=mode, sum_out=s, sum_out_f64=s64)
         torch.cuda.synchronize()
-        o, sv = out.cpu().numpy(), s.cpu().numpy()
-        rows_to_check = range(R) if R <= 64 else np.random.default_rng(i).integers(0, R, 64)
-        for r in rows_to_check:
-            check(x[r, :C], o[r, :C], sv[r], mode, d)
+        o, sv, sv64 = out.cpu().numpy(), s.cpu().numpy(), s64.cpu().numpy()
+        xc = np.ascontiguousarray(x[:, :C])
+        S = oracle.rows_sum_exact(xc)  # every row's own exact sum
+        scale = oracle.rows_sum_exact(np.abs(xc)) if d == 3 else np.abs(S)
+        bad = np.nonzero(np.abs(sv.astype(np.float64) - S) > 1e-6 * scale)[0]
+        assert bad.size == 0, (R, C, bad[:5], sv[bad[:5]], S[bad[:5]])
+        assert np.all(np.abs(sv64 - S) <= 1e-6 * scale)  # the fp64 S_r as accumulated
+        cov = oracle.covered_mask(C, mode)
+        # bitwise replay of every covered element of every row with its own divisor
+        q = xc[:, cov] / sv[:, None]
+        assert np.array_equal(o[:, :C][:, cov].view(np.uint32), q.view(np.uint32))
+        assert np.all(o[:, :C][:, ~cov].view(np.uint32) == SENTINEL_BITS)
         assert np.all(o[:, C:].view(np.uint32) == SENTINEL_BITS)
-        if R > 64:  # full-size config: replay every row with its own divisor
-            cov = oracle.covered_mask(C, mode)
-            q = x[:, :C][:, cov] / sv[:, None]
-            assert np.array_equal(o[:, :C][:, cov], q)
-            assert np.all(o[:, :C][:, ~cov].view(np.uint32) == SENTINEL_BITS)
+        # per-element 1e-5 against the oracle's rows form (positive inputs)
+        if d != 3:
+            ref = oracle.rows(xc, mode, out=np.zeros_like(xc))[:, cov].astype(np.float64)
+            got = o[:, :C][:, cov].astype(np.float64)
+            nz = ref != 0
+            assert np.all(np.abs(got[nz] - ref[nz]) <= 1e-5 * np.abs(ref[nz]))
+            assert np.all(got[~nz] == 0)
+        if R <= 64:  # small shapes: the full per-row check (replay against oracle_replay)
+            for r in range(R):
+                check(xc[r], o[r, :C], sv[r], mode, d)
 
 
 @pytest.mark.parametrize("mode", ["literal", "dense"])
@@ -449,23 +478,40 @@ def test_sharded_multirange_local_semantics():
 
 
 def test_torch_ops():
+    """NEXT-3: torch.ops.libnorm.* against the ORACLE (not against libnorm)."""
     import paper_2207_00257_b200.torch_ops as T
-    x = to_dev(gen.make_host(3 * 2**20 + 5, seed=3, dist=0))
-    y = torch.ops.libnorm.normalize(x, "dense")
-    ref = torch.empty_like(x)
-    L.normalize(ref, x, index="dense")
-    torch.cuda.synchronize()
-    assert torch.equal(y, ref)
-    assert torch.allclose(y, (x.double() / x.double().sum()).float(), rtol=1e-5, atol=0)
-    z = torch.ops.libnorm.normalize(x, "literal")  # uncovered elements keep x
-    c, p = L.coverage(x.numel())
-    assert torch.equal(z[p:], x[p:]) and torch.equal(z[:p], ref[:p] * 0 + z[:p])
+    n = 3 * 2**20 + 5
+    xh = gen.make_host(n, seed=3, dist=0)
+    x = to_dev(xh)
+    S = oracle.sum_exact(xh)
+    for mode in ("dense", "literal"):
+        y = torch.ops.libnorm.normalize(x, mode)
+        torch.cuda.synchronize()
+        yh = y.cpu().numpy()
+        cov = oracle.covered_mask(n, mode)
+        # covered outputs: within 1e-5 of the oracle's form 3 (exact S, fp64 quotient)
+        ref = oracle.normalize(xh, mode, out=xh.copy())
+        assert np.all(np.abs(yh[cov].astype(np.float64) - ref[cov]) <= 1e-5 * ref[cov])
+        # uncovered outputs: x's bits (the op applies Fig. 1 in place to a copy)
+        assert np.array_equal(yh[~cov].view(np.uint32), xh[~cov].view(np.uint32))
+        # and the whole output is the oracle's binary32 replay for ONE divisor s
+        # within 1e-6 of S: recover s from an element (x / y), then replay
+        i = int(np.nonzero(cov)[0][-1])
+        cands = [np.float32(v) for v in (np.float32(S), np.nextafter(np.float32(S), np.float32(0)),
+                                         np.nextafter(np.float32(S), np.float32(np.inf)))]
+        cands += [np.float32(xh[i] / yh[i])]
+        ok = [c for c in cands if abs(float(c) - S) <= 1e-6 * S and
+              np.array_equal(oracle.replay(xh, c, mode, out=xh.copy()).view(np.uint32), yh.view(np.uint32))]
+        assert ok, "no divisor within 1e-6 of S replays the op's output"
+        x2 = x.clone()
+        torch.ops.libnorm.normalize_(x2, mode)  # in place: the same bits
+        assert torch.equal(x2, y)
     m = to_dev(gen.make_host(64 * 4096, seed=4, dist=0).reshape(64, 4096))
     r = T.Normalize("dense")(m)
     assert torch.allclose(r, (m.double() / m.double().sum(-1, keepdim=True)).float(), rtol=1e-5, atol=0)
-    w = m.clone()
-    torch.ops.libnorm.normalize_(w, "dense")
-    assert torch.allclose(w.sum(), torch.tensor(1.0, device="cuda"), rtol=1e-5)
+    mh = m.cpu().numpy()
+    refr = oracle.rows(mh, "dense")
+    assert np.all(np.abs(r.cpu().numpy().astype(np.float64) - refr) <= 1e-5 * refr)
     f = torch.compile(lambda t: torch.ops.libnorm.normalize_rows(t * 2.0, "dense"), fullgraph=True)
     assert torch.allclose(f(m), r, rtol=1e-6, atol=0)
     with pytest.raises(RuntimeError):
@@ -474,8 +520,9 @@ def test_torch_ops():
     lg = to_dev(gen.make_host(96 * 4096, seed=5, dist=3).reshape(96, 4096)) * 8
     sm = torch.ops.libnorm.softmax(lg, False)
     ls = torch.ops.libnorm.softmax(lg, True)
-    assert torch.allclose(sm, torch.softmax(lg.double(), 1).float(), rtol=1e-5, atol=1e-37)
-    assert torch.allclose(ls, torch.log_softmax(lg.double(), 1).float(), rtol=1e-5, atol=1e-5)
+    lgh = lg.cpu().numpy()
+    assert torch.allclose(sm.cpu(), torch.from_numpy(oracle.softmax_rows(lgh)), rtol=1e-5, atol=1e-37)
+    assert torch.allclose(ls.cpu(), torch.from_numpy(oracle.softmax_rows(lgh, log=True)), rtol=1e-5, atol=1e-5)
     g = torch.compile(lambda t: torch.ops.libnorm.softmax(t, False), fullgraph=True)
     assert torch.equal(g(lg), sm)
 

@@ -343,3 +343,43 @@ def test_json_cli_spec_example():
     lit = json.loads(r.stdout)["buffers"]["out"]
     assert lit[0] == float(np.float32(1 / 36)) and all(v is None for v in lit[1:])
     assert subprocess.run([sys.executable, "-m", "oracle", "{bad"], capture_output=True, cwd=ROOT).returncode == 1
+
+
+# ----------------------------------------- threaded form 3 and per-row sums
+
+@pytest.mark.parametrize("mode", ["literal", "dense"])
+def test_form_hoisted_mt_bit_identical(mode):
+    """The cpu_baseline timer (form 3 on T threads, chunk accumulators merged
+    exactly) equals form 3 bit for bit, for every T, including the wide-exponent
+    (D4) and signed (D3) inputs where a per-thread fp64 merge would differ, the
+    non-finite classification (R7), and the residue coverage of G < 32."""
+    rng = np.random.default_rng(7)
+    for n in (1, 7, 33, 100, 992, 1025, 4099, 2**16 + 3, 2**20 + 7):
+        for d in (0, 3, 4):
+            x = gen.make_host(n, seed=int(rng.integers(1 << 30)), dist=d)
+            ref, adds = oracle.form_hoisted(x, mode, out=np.full(n, 7.0, np.float32))
+            for T in (1, 2, 3, 16, 64):
+                got, a2 = oracle.form_hoisted_mt(x, mode, threads=T, out=np.full(n, 7.0, np.float32))
+                assert a2 == adds == n
+                assert got.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes(), (n, d, T)
+    # wide dynamic range split across threads: 2^100 + 1 - 2^100 must give 1 exactly
+    x = np.array([2.0**100, 1.0, -(2.0**100), 1.0], np.float32)
+    got, _ = oracle.form_hoisted_mt(x, "dense", threads=4)
+    assert np.array_equal(got, x / np.float32(2.0))
+    for special, expect in (([np.inf, 1.0], np.inf), ([np.inf, -np.inf], np.nan), ([np.nan, 1.0], np.nan)):
+        xs = np.array(special * 8, np.float32)
+        got, _ = oracle.form_hoisted_mt(xs, "dense", threads=5)
+        ref, _ = oracle.form_hoisted(xs, "dense")
+        assert got.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes()
+    with pytest.raises(ValueError):
+        oracle.form_hoisted_mt(x, "dense", threads=0)
+
+
+def test_rows_sum_exact_matches_fsum():
+    """Per-row exact sums == math.fsum of each row (exact, correctly rounded)."""
+    x = gen.make_host(37 * 129, seed=3, dist=4).reshape(37, 129)
+    S = oracle.rows_sum_exact(x)
+    for r in range(37):
+        assert S[r] == _fsum(x[r])
+    # integer closed form: const rows of length c sum to c
+    assert np.all(oracle.rows_sum_exact(np.ones((5, 4096), np.float32)) == 4096)
