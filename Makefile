@@ -28,7 +28,10 @@ $(PKG)/libnorm.so: $(CSRC) $(CHDR)
 	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
 # Plain-C consumer of the C ABI (no Python): examples/normalize_c
-examples: examples/normalize_c
+examples: examples/normalize_c examples/latency_c
+examples/latency_c: examples/latency_c.c include/libnorm.h $(PKG)/libnorm.so
+	$(CC) -std=c11 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -l:libnorm.so \
+	    -L/usr/local/cuda/lib64 -lcudart -lm -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 examples/normalize_c: examples/normalize_c.c include/libnorm.h $(PKG)/libnorm.so
 	$(CC) -std=c11 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -l:libnorm.so \
 	    -L/usr/local/cuda/lib64 -lcudart -lm -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64

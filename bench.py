@@ -9,7 +9,9 @@ per rank, plus one 8-byte ncclAllGather when N > 1.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vector|rows|fused28]
                   [--index literal|dense] [--impl libnorm|reference]
 
-For N > 1 launch with torchrun (one process per GPU).  Rank 0 prints ONE JSON line.
+For N > 1 the driver launches it under torchrun (one process per GPU); a plain
+`python bench.py --gpus N` re-executes itself under torch.distributed.run with N
+ranks.  Rank 0 prints ONE JSON line.
 value = algorithmic bytes of the whole job (4n + 8|C(n)|) per second
 of the max-over-ranks device time.  Inputs (16 GiB at n = 2^32) are far larger than
 the 126 MB L2, so no flush is needed between steps (the rows / 2^28 workloads flush).
@@ -131,25 +133,80 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(index, n_sample=2**28, reps=10):
-    """Time the CPU oracle (form 3, hoisted O(N)) as it stands, single-threaded,
-    on a bounded sample of the same workload; returns GB/s of algorithmic bytes."""
+def oracle_bytes(n, index):
+    """Algorithmic bytes 4n + 8|C(n)| from the ORACLE's closed-form coverage (the
+    reference arm never loads the product library)."""
+    import oracle
+    count, _ = oracle.coverage_closed(n, index)
+    return 4 * n + 8 * count
+
+
+def oracle_sample(index, n_sample=2**28, reps=5):
+    """Time the CPU oracle (form 3, hoisted O(N): exact sum, then the scale of
+    C(n)) as it stands on a bounded sample of the same workload, on all of the
+    host's cores (oracle_form_hoisted_mt: contiguous chunks accumulated exactly,
+    merged in chunk order -- bit-identical to the single-thread form 3) and on one
+    thread (the form as written); returns GB/s of algorithmic bytes."""
     import gen
     import oracle
-    import paper_2207_00257_b200 as L
     x = gen.make_host(n_sample, seed=2207, dist="unit")
     out = x.copy()
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        oracle.form_hoisted(x, index, out=out)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    b = L.algorithmic_bytes(n_sample, index)
-    return {"value": b / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle form 3 (hoisted sum + scale, fp64 exact sum), n={n_sample} "
-                      f"{index} index, median of {reps}, {t:.3f} s each, 1 thread of "
-                      f"{os.cpu_count()} ({cpu_model()})"}
+    T = os.cpu_count() or 1
+    b = oracle_bytes(n_sample, index)
+
+    def med(fn, k):
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+    tT = med(lambda: oracle.form_hoisted_mt(x, index, threads=T, out=out), reps)
+    t1 = med(lambda: oracle.form_hoisted(x, index, out=out), 3)
+    return {"value": b / tT / 1e9, "unit": "GB/s", "cores": T, "kind": "oracle",
+            "sample": f"oracle form 3 (exact sum of all n, then in[i]/val over C(n)), n={n_sample} "
+                      f"{index} index, {T} threads (contiguous chunks, exact chunk-order merge), "
+                      f"median of {reps}: {tT:.3f} s; {cpu_model()}",
+            "single_thread": {"value": b / t1 / 1e9, "unit": "GB/s", "cores": 1,
+                              "sample": f"same sample, oracle_form_hoisted (1 thread), median of 3: {t1:.3f} s"}}
+
+
+def run_meta(world=1):
+    """Versions of everything the number depends on (SURVEY §5 run metadata;
+    PAPER.md:770-774 records its own machine and versions)."""
+    import ctypes
+    import platform
+    m = {"torch": None, "cuda_runtime": None, "gpu": None, "driver": None, "nccl_libnorm": None,
+         "nccl_torch": None, "host_cpu": cpu_model(), "host_cores": os.cpu_count(),
+         "python": platform.python_version(), "world_size": world}
+    try:
+        import torch
+        m["torch"] = torch.__version__
+        m["cuda_runtime"] = torch.version.cuda
+        if torch.cuda.is_available():
+            m["gpu"] = torch.cuda.get_device_name()
+            cc = torch.cuda.get_device_capability()
+            m["sm"] = f"sm_{cc[0]}{cc[1]}"
+        try:
+            v = torch.cuda.nccl.version()
+            m["nccl_torch"] = ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+        except Exception:  # noqa: BLE001
+            pass
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        v = ctypes.c_int()
+        ctypes.CDLL("libnccl.so.2").ncclGetVersion(ctypes.byref(v))  # the one libnorm.so links (rpath)
+        m["nccl_libnorm"] = f"{v.value // 10000}.{(v.value % 10000) // 100}.{v.value % 100}"
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        r = subprocess.run(["nvidia-smi", "--query-gpu=driver_version", "--format=csv,noheader"],
+                           capture_output=True, text=True, timeout=20)
+        m["driver"] = r.stdout.strip().splitlines()[0] if r.returncode == 0 and r.stdout.strip() else None
+    except Exception:  # noqa: BLE001
+        pass
+    return m
 
 
 # --------------------------------------------------------------------------- arms
@@ -237,6 +294,9 @@ def workload_name(n, index):
 
 
 def run_reference(args):
+    """The reference arm for this tier: the CPU oracle (form 3) as it stands, on
+    all host cores, over a bounded sample of the workload per step.  Loads only
+    oracle/ and gen/ -- never the product library."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -245,17 +305,17 @@ def run_reference(args):
     steps = []
     import gen
     import oracle
-    import paper_2207_00257_b200 as L
+    T = os.cpu_count() or 1
     x = gen.make_host(n_sample, seed=2207, dist="unit")
     out = x.copy()
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.form_hoisted(x, args.index, out=out)
+        oracle.form_hoisted_mt(x, args.index, threads=T, out=out)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             steps.append(dt)
     ms = 1e3 * sum(steps) / len(steps)
-    b = L.algorithmic_bytes(n_sample, args.index)
+    b = oracle_bytes(n_sample, args.index)
     v = b / (ms / 1e3) / 1e9
     line = {
         "impl": "reference", "metric": "normalize GB/s and % of HBM peak, n=2^32 fp32, at 1/2/4/8 B200",
@@ -266,11 +326,216 @@ def run_reference(args):
                    "sample": f"CPU oracle (form 3, hoisted) on a bounded sample: n={n_sample} per step; "
                              f"value = the sample's algorithmic bytes / its time",
                    "n": args.n, "sample_n": n_sample, "index": args.index},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"n={n_sample} per step, 1 thread of {os.cpu_count()} ({cpu_model()})"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": T, "kind": "oracle",
+                         "sample": f"n={n_sample} per step, oracle_form_hoisted_mt on {T} threads "
+                                   f"(exact chunk accumulators; bit-identical to form 3) ({cpu_model()})"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "meta": {"host_cpu": cpu_model(), "host_cores": T, "world_size": world,
+                 "note": "oracle only: loads oracle/liboracle.so and gen/libnormgen.so, not libnorm.so"},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+def min_over_ranks(v, world):
+    return -max_over_ranks(-v, world)
+
+
+def _emulated():
+    """N > 1 ranks time-slicing one GPU over gloo (harness tests only): NCCL
+    refuses two ranks on one device, so the NCCL exchanges are not run."""
+    return os.environ.get("NORM_BENCH_BACKEND", "nccl") != "nccl"
+
+
+def make_exchange(L, name, world):
+    """A libnorm communicator for one of the N > 1 exchanges, or None for the
+    caller-collective path ("host")."""
+    if name == "p2p":
+        return L.PeerComm()
+    if name in ("nccl", "nccl-allreduce"):
+        return L.Comm(allreduce=name == "nccl-allreduce")
+    return None
+
+
+def sharded_step_fn(L, comm, out, inp, mine, n, index, world, path="auto"):
+    if comm is None:
+        ag = host_all_gather(world)
+        return lambda ev=None: L.normalize_sharded_via(out, inp, mine, n, ag, index=index, events=ev)
+    if isinstance(comm, L.PeerComm):
+        return lambda ev=None: comm.normalize_sharded(out, inp, mine, n, index=index, events=ev, path=path)
+    return lambda ev=None: comm.normalize_sharded(out, inp, mine, n, index=index, events=ev)
+
+
+def time_steps(step, steps, world, flush=None):
+    """Device time per step (ms, this rank): K steps bracketed by barrier + sync.
+    Without flush: one event pair around the K back-to-back steps.  With flush:
+    the L2 flush runs between steps, outside per-step event pairs."""
+    import torch
+    stream = torch.cuda.current_stream()
+    barrier(world)
+    if flush is None:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        return a.elapsed_time(b) / steps
+    per = []
+    for _ in range(steps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        per.append(a.elapsed_time(b))
+    barrier(world)
+    return sum(per) / len(per)
+
+
+def reduce_times(step, steps, world, flush=None):
+    """Average duration of the step's dominant kernel (norm_debug_set_events on the
+    launch stream) and of the instrumented step, in a separate pass: an event
+    between the reduce and the scale would defeat their programmatic dependent
+    launch, so the headline steps carry none.  With flush: L2 flushed before
+    every step, outside the step's events."""
+    import torch
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(world)
+    if flush is None:
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record(stream)
+        for k in range(steps):
+            step(evs[k])
+        i1.record(stream)
+        torch.cuda.synchronize()
+        instr = i0.elapsed_time(i1) / steps
+    else:
+        per = []
+        for k in range(steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(evs[k])
+            b.record(stream)
+            torch.cuda.synchronize()
+            per.append(a.elapsed_time(b))
+        instr = sum(per) / len(per)
+    barrier(world)
+    red = [b.elapsed_time(e) for b, e in evs]
+    return sum(red) / len(red), instr
+
+
+def exchange_record(L, name, out, inp, mine, n, index, world, args, flush):
+    """The same sharded step through another exchange (N > 1): step time (max
+    and min over ranks), the dominant kernel's time, and the rest (exchange +
+    scale, or the fused kernel's own exchange inside it)."""
+    comm = make_exchange(L, name, world)
+    try:
+        step = sharded_step_fn(L, comm, out, inp, mine, n, index, world)
+        for _ in range(args.warmup):
+            step()
+        ms_local = time_steps(step, args.steps, world, flush)
+        red, instr = reduce_times(step, args.steps, world, flush)
+        algo = L.algorithmic_bytes(n, index)
+        ms = max_over_ranks(ms_local, world)
+        return {"exchange": name, "value": algo / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                "rank_ms_min": min_over_ranks(ms_local, world), "rank_ms_max": ms,
+                "dominant_kernel_ms_max": max_over_ranks(red, world),
+                "rest_of_step_ms_max": max_over_ranks(instr - red, world)}
+    finally:
+        if comm is not None:
+            comm.destroy()
+
+
+def exchange_latency(L, names, world, index, reps=200):
+    """Latency of one sharded normalize over a tiny vector (8192 elements per
+    rank: the kernels are launch-bound, so the step is launch + exchange +
+    launch), per exchange, max over ranks -- the cost the exchange adds to a
+    step, measured on the device."""
+    import torch
+    n = 8192 * world
+    mine = L.plan_shards(n, world, index, True)[torch.distributed.get_rank()]
+    nl = sum(ln for _, ln in mine)
+    inp = torch.ones(nl, device="cuda")
+    out = torch.empty_like(inp)
+    res = {}
+    for name in names:
+        comm = make_exchange(L, name, world)
+        try:
+            step = sharded_step_fn(L, comm, out, inp, mine, n, index, world)
+            for _ in range(10):
+                step()
+            ms = time_steps(step, reps, world)
+            res[name] = {"us_per_step_max": 1e3 * max_over_ranks(ms, world),
+                         "us_per_step_min": 1e3 * min_over_ranks(ms, world)}
+        except Exception as e:  # noqa: BLE001
+            res[name] = {"unavailable": str(e)[:200]}
+        finally:
+            if comm is not None:
+                comm.destroy()
+    res["n_per_rank"] = nl
+    return res
+
+
+def parity_record(L, out, inp, n, index, sentinel_bits):
+    """Parity of the benched launch (N = 1) against the oracle, on the bench's own
+    buffers (SURVEY §5 'parity status in the JSON line'): one extra call with
+    sum_out; s vs the oracle's exact sum of all n inputs (oracle_sum_exact_mt
+    over a host copy); 2^20 sampled covered outputs
+    replayed bitwise (in[i] / s in binary32) and within 1e-5 of in[i] / S; 2^16
+    sampled uncovered outputs still hold the sentinel."""
+    import numpy as np
+    import torch
+    import oracle
+    nl = inp.numel()
+    need = 4 * nl
+    try:
+        avail = 0
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                avail = int(line.split()[1]) * 1024
+        if avail and avail < 3 * need:
+            return {"ok": None, "skipped": f"host MemAvailable {avail >> 30} GiB < 3 x {need >> 30} GiB shard"}
+    except OSError:
+        pass
+    s = torch.zeros(1, device="cuda")
+    L.normalize(out, inp, index=index, sum_out=s)
+    torch.cuda.synchronize()
+    x = np.empty(nl, dtype=np.float32)
+    step = 1 << 28
+    for a in range(0, nl, step):
+        x[a:a + step] = inp[a:a + step].cpu().numpy()
+    S = oracle.sum_exact_mt(x)
+    sv = np.float32(s.item())
+    rel_s = abs(float(sv) - S) / abs(S)
+    count, prefix = oracle.coverage_closed(n, index)
+    rng = np.random.default_rng(2207)
+    if prefix >= 0:
+        ci = rng.integers(0, prefix, 1 << 20) if prefix > 0 else np.zeros(0, np.int64)
+        ui = rng.integers(prefix, n, 1 << 16) if prefix < n else np.zeros(0, np.int64)
+    else:
+        mask = oracle.covered_mask(n, index)
+        ci = rng.choice(np.nonzero(mask)[0], 1 << 20)
+        ui = rng.choice(np.nonzero(~mask)[0], 1 << 16) if (~mask).any() else np.zeros(0, np.int64)
+    idx = torch.from_numpy(np.concatenate([ci, ui])).cuda()
+    o = out[idx].cpu().numpy()
+    oc, ou = o[:ci.size], o[ci.size:]
+    replay = bool(np.array_equal(oc.view(np.uint32), (x[ci] / sv).view(np.uint32)))
+    ref = x[ci].astype(np.float64) / S
+    max_rel = float(np.max(np.abs(oc - ref) / ref)) if ci.size else 0.0
+    untouched = bool(np.all(ou.view(np.uint32) == sentinel_bits))
+    ok = rel_s <= 1e-6 and replay and max_rel <= 1e-5 and untouched
+    del x
+    return {"ok": ok, "s": float(sv), "S_exact": S, "rel_err_s": rel_s, "tol_s": 1e-6,
+            "covered_sampled": int(ci.size), "replay_bitwise": replay, "max_rel_err": max_rel, "tol": 1e-5,
+            "uncovered_sampled": int(ui.size), "uncovered_untouched": untouched,
+            "oracle": "oracle_sum_exact_mt (exact superaccumulator) over all n inputs on the host"}
+
+
+SENTINEL_BITS = 0x7FC0FFEE
 
 
 def run_vector(args, world, rank, local):
@@ -288,8 +553,16 @@ def run_vector(args, world, rank, local):
     for b, ln in mine:  # each rank generates its own global ranges in HBM
         gen.fill_cuda(inp[off:off + ln], seed=2207, dist="unit", offset=b)
         off += ln
+    # uncovered outputs are never written: prefill a sentinel so parity can see that
     out = torch.empty_like(inp)
+    out.view(torch.int32).fill_(SENTINEL_BITS)
     torch.cuda.synchronize()
+    l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+    # Timing rule: inputs larger than L2 or an L2 flush between timed steps.
+    flush = None if 4 * nloc >= 4 * l2 else L2Flush()
+    l2_note = (f"no flush: {4 * nloc / 2**30:.2f} GiB input per GPU >= 4 x L2 ({l2 >> 20} MiB)" if flush is None
+               else f"L2 flushed before every step (256 MiB write + 256 MiB read, outside the per-step "
+                    f"events): {4 * nloc / 2**20:.1f} MiB input per GPU < 4 x L2")
     comm = None
     exchange_note = None
     if world > 1 and args.exchange == "p2p":
@@ -315,48 +588,23 @@ def run_vector(args, world, rank, local):
             args.exchange = "nccl"
     if world > 1 and args.exchange in ("nccl", "nccl-allreduce") and comm is None:
         comm = L.Comm(allreduce=args.exchange == "nccl-allreduce")
-    ag = host_all_gather(world) if world > 1 and args.exchange == "host" else None
     stream = torch.cuda.current_stream()
 
-    def step(ev=None):
-        if world == 1:
+    if world == 1:
+        def step(ev=None):
             L.normalize(out, inp, index=index, path=args.path, events=ev)
-        elif comm is not None:
-            comm.normalize_sharded(out, inp, mine, n, index=index, events=ev)
-        else:
-            L.normalize_sharded_via(out, inp, mine, n, ag, index=index, events=ev)
+    else:
+        step = sharded_step_fn(L, comm, out, inp, mine, n, index, world)
 
     for _ in range(args.warmup):
         step()
-    # Timed region: K whole steps, bracketed by barrier + sync.  The reduce
-    # kernel's own duration is taken in a second, instrumented pass (events
-    # recorded by libnorm around the reduce launch, on the launch stream),
-    # because an event between the two kernels disables their programmatic
-    # dependent launch and would perturb the step being timed.
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # Timed region: K whole steps, bracketed by barrier + sync.
     barrier(world)
     with ClockSampler(local) as clk:
-        t0.record(stream)
-        for k in range(args.steps):
-            step()
-        t1.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_local = t0.elapsed_time(t1) / args.steps
+        ms_local = time_steps(step, args.steps, world, flush)
     ms = max_over_ranks(ms_local, world)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    i0.record(stream)
-    for k in range(args.steps):
-        step(evs[k])
-    i1.record(stream)
-    torch.cuda.synchronize()
-    barrier(world)
-    ms_instr = i0.elapsed_time(i1) / args.steps
-    red_ms = [b.elapsed_time(e) for b, e in evs]
-    red_ms_avg = sum(red_ms) / len(red_ms)
+    ms_min = min_over_ranks(ms_local, world)
+    red_ms_avg, ms_instr = reduce_times(step, args.steps, world, flush)
     algo = L.algorithmic_bytes(n, index)
     value = algo / (ms / 1e3) / 1e9
     peak, peak_src = load_peak()
@@ -372,7 +620,8 @@ def run_vector(args, world, rank, local):
     else:
         kpath = "two_pass"
     fused_step = kpath == "fused"
-    red_bytes = 4 * nloc + (8 * lloc if fused_step else 0)
+    small_step = kpath == "small"
+    red_bytes = 4 * nloc + (8 * max(lloc, 0) if (fused_step or small_step) else 0)
     # in-run calibration on the same buffers: a torch copy stream
     # (read + write bytes) and a torch read-only stream (torch.sum)
     calib = {}
@@ -386,8 +635,10 @@ def run_vector(args, world, rank, local):
             b.record(stream)
             torch.cuda.synchronize()
             return a.elapsed_time(b) / reps
-        cms = _t(lambda: out.copy_(inp))
+        scratch = torch.empty_like(inp)
+        cms = _t(lambda: scratch.copy_(inp))
         rms = _t(lambda: torch.sum(inp))
+        del scratch
         calib = {"torch_copy_gbs": 8 * nloc / (cms / 1e3) / 1e9, "torch_sum_gbs": 4 * nloc / (rms / 1e3) / 1e9,
                  "note": "same-run torch streams on this rank's buffers (copy counts read+write bytes)"}
     achieved = red_bytes / (red_ms_avg / 1e3) / 1e9
@@ -406,53 +657,73 @@ def run_vector(args, world, rank, local):
     per = sorted(sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps))
     stats = {"median_ms": max_over_ranks(statistics.median(per), world),
              "min_ms": max_over_ranks(per[0], world),
-             "p90_ms": max_over_ranks(per[min(len(per) - 1, int(0.9 * len(per)))], world)}
+             "p90_ms": max_over_ranks(per[min(len(per) - 1, int(0.9 * len(per)))], world),
+             "rank_ms_min": ms_min, "rank_ms_max": ms}
     if world == 1:
         g = L.NormGraph(out, inp, index=index, path=args.path)
         for _ in range(2):
             g.launch()
-        barrier(world)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            g.launch()
-        b.record(stream)
-        torch.cuda.synchronize()
-        gms = a.elapsed_time(b) / args.steps
+        gms = time_steps(g.launch, args.steps, world, flush)
         stats["graph_ms_per_step"] = gms
         stats["graph_value"] = L.algorithmic_bytes(n, index) / (gms / 1e3) / 1e9
         g.destroy()
     extra["step_stats"] = stats
+    # N > 1: the same step through the other exchanges, so one driver run measures
+    # the north_star's NCCL all-reduce of the scalar beside the fused peer exchange
+    if world > 1:
+        alt = {}
+        for name in ("nccl-allreduce", "nccl", "p2p", "host"):
+            if name == args.exchange or (name.startswith("nccl") and _emulated()):
+                continue
+            try:
+                alt[name] = exchange_record(L, name, out, inp, mine, n, index, world, args, flush)
+            except Exception as e:  # noqa: BLE001
+                alt[name] = {"exchange": name, "unavailable": str(e)[:300]}
+        if _emulated():
+            alt["note"] = "ranks time-slice one GPU over gloo: NCCL exchanges not run (NCCL needs one GPU per rank)"
+        extra["exchanges"] = alt
+        if "nccl-allreduce" in alt:
+            extra["nccl_allreduce"] = alt["nccl-allreduce"]
+        names = ["p2p", "host"] + ([] if _emulated() else ["nccl-allreduce", "nccl"])
+        extra["exchange_latency"] = exchange_latency(L, names, world, index)
     # dense-index figure on the same buffers (caption reading R1), reported beside the headline
     if args.also_dense and index == "literal" and (world == 1 or comm is not None):
         dense_mine = L.plan_shards(n, world, "dense", True)[rank]
         if dense_mine == mine or world == 1:
+            if world == 1:
+                def dstep():
+                    L.normalize(out, inp, index="dense", path="auto")
+            else:
+                dstep = sharded_step_fn(L, comm, out, inp, mine, n, "dense", world)
             for _ in range(2):
-                L.normalize(out, inp, index="dense", path="auto") if comm is None else \
-                    comm.normalize_sharded(out, inp, mine, n, index="dense")
-            barrier(world)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(args.steps):
-                L.normalize(out, inp, index="dense", path="auto") if comm is None else \
-                    comm.normalize_sharded(out, inp, mine, n, index="dense")
-            b.record(stream)
-            torch.cuda.synchronize()
-            dms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+                dstep()
+            dms = max_over_ranks(time_steps(dstep, args.steps, world, flush), world)
             dbytes = L.algorithmic_bytes(n, "dense")
             extra["dense_index"] = {"value": dbytes / (dms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": dms,
                                     "frac_of_peak": dbytes / (dms / 1e3) / 1e9 / (world * peak)}
+            out.view(torch.int32).fill_(SENTINEL_BITS)  # dense wrote every element: restore the sentinel
+            for _ in range(1):
+                step()
+            torch.cuda.synchronize()
     # e2e: same metric through the public API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, world, rank, local, mine, n, index)
-    launches_per_step = 1 if fused_step else 2
+    parity = None
+    if not args.no_parity and world == 1:
+        parity = parity_record(L, out, inp, n, index, SENTINEL_BITS)
+    launches_per_step = 1 if (fused_step or small_step) else 2
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(index)
+    meta = run_meta(world)
     if rank != 0:
         return
     cov_count, prefix = L.coverage(n, index)
+    kname = ("fused_kernel (reduce + grid barrier + exchange + scale: the whole step)" if fused_step else
+             "small_kernel (one CTA: sum, barrier, scale: the whole step)" if small_step else
+             ("reduce_dyn_kernel (TMA-bulk reduce, dynamic deterministic tail)" if nloc >= (1 << 22)
+              else "reduce_kernel") + " (the hoisted sum: 4n of the step's 4n + 8|C| bytes)")
     line = {
         "metric": "normalize GB/s and % of HBM peak, n=2^32 fp32, at 1/2/4/8 B200",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -469,31 +740,30 @@ def run_vector(args, world, rank, local):
                    "shard_plan": (("coverage-balanced two-range" if args.plan == "balanced" else "uniform one-range")
                                   if world > 1 else None),
                    "exchange_note": exchange_note, "inputs": "seeded synthetic D0 unit grid (gen/), generated in HBM",
-                   "l2": f"no flush: {4 * nloc / 2**30:.1f} GiB input per GPU >> 126 MB L2"},
+                   "l2": l2_note},
         "frac_of_hbm_peak": value / (world * peak),
         "frac_of_datasheet": value / (world * DATASHEET_GBS),
         "calibration": calib,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
-                     "kernel": ("fused_kernel (reduce + grid barrier + exchange + scale: the whole step)"
-                                if fused_step else
-                                ("reduce_dyn_kernel (TMA-bulk reduce, dynamic deterministic tail)"
-                                 if nloc >= (1 << 22) else "reduce_kernel")
-                                + " (the hoisted sum: 94% of the literal step's bytes)"),
+                     "kernel": kname,
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_instr, "instrumented_ms_per_step": ms_instr,
                      "frac_of_same_run_read_stream": (achieved / calib["torch_sum_gbs"]) if calib else None,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
+        "meta": meta,
     }
     line.update(extra)
+    if parity is not None:
+        line["parity"] = parity
     if e2e:
         line["e2e"] = e2e
     if cpu:
         line["cpu_baseline"] = cpu
-    print(json.dumps(line), flush=True)
+    emit(line)
     if comm:
         comm.destroy()
 
@@ -651,7 +921,7 @@ def run_rows(args, world, rank, local):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_paths28(args, world, rank, local):
@@ -691,7 +961,7 @@ def run_paths28(args, world, rank, local):
                        "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "paths": res, "peak": peak, "gpu_launches": args.steps}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_softmax(args, world, rank, local):
@@ -771,7 +1041,7 @@ def run_softmax(args, world, rank, local):
             "frac_of_hbm_peak": res["softmax"]["frac"], "peak": peak, "results": res,
             "gpu_launches": args.steps}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_backprop(args, world, rank, local):
@@ -819,7 +1089,118 @@ def run_backprop(args, world, rank, local):
             "speedup_tma_over_printed": res["printed"]["ms_per_step"] / res["tma"]["ms_per_step"],
             "gpu_launches": args.steps * len(res)}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
+
+
+def run_small(args, world, rank, local):
+    """BASELINE configs[0] and configs[1] ("latency-bound (us)",
+    "report us hot and with L2 flushed"): n = 1024 (Fig. 1's 32 x 32 literal
+    grid) and n = 2^20 + 7 (ragged: literal coverage leaves
+    outputs untouched), on every path.  Per path and size:
+      device_hot_us    -- one CUDA graph of R back-to-back calls, replayed; device
+                          time / R (no host in the loop);
+      device_flushed_us-- graph of R x (L2 flush + call) minus graph of R x flush,
+                          / R: the call with its input evicted from L2;
+      python_us        -- back-to-back calls through the Python binding
+                          (trusted pointers), wall time / call;
+      c_*              -- examples/latency_c: host enqueue and back-to-back wall
+                          time per call from plain C, with and without libnorm's
+                          pointer checks, and through a norm_graph_t replay;
+      parity           -- each path's output vs the oracle (exact S within 1e-6,
+                          bitwise replay, uncovered outputs untouched)."""
+    import numpy as np
+    import torch
+    import gen
+    import oracle
+    import paper_2207_00257_b200 as L
+    stream = torch.cuda.current_stream()
+    ws = torch.zeros(L.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    R = 100
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_r = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_w.zero_()
+        flush_r.sum()
+
+    def graph_us(body, reps=10):
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            body()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                body()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3 / reps
+
+    res = []
+    ok_all = True
+    for n in (1024, 2**20 + 7):
+        xh = gen.make_host(n, seed=2207, dist="unit")
+        x = torch.from_numpy(xh).cuda()
+        out = torch.empty_like(x)
+        count, prefix = L.coverage(n, args.index)
+        t_flush = graph_us(lambda: [flush() for _ in range(20)]) / 20
+        for path in ("auto", "small", "two_pass", "fused"):
+            chosen = L.choose_path(n, prefix, path)
+
+            def call():
+                L.normalize(out, x, index=args.index, path=path, workspace=ws, trusted=True)
+            # parity of this path (sentinel-filled output, then one call)
+            out.view(torch.int32).fill_(SENTINEL_BITS)
+            s = torch.zeros(1, device="cuda")
+            L.normalize(out, x, index=args.index, path=path, workspace=ws, sum_out=s)
+            torch.cuda.synchronize()
+            o, sv, S = out.cpu().numpy(), np.float32(s.item()), oracle.sum_exact(xh)
+            sent = np.full(n, SENTINEL_BITS, np.uint32).view(np.float32)
+            rep = oracle.replay(xh, sv, args.index, out=sent.copy())
+            ok = abs(float(sv) - S) <= 1e-6 * S and np.array_equal(o.view(np.uint32), rep.view(np.uint32))
+            ok_all &= bool(ok)
+            hot = graph_us(lambda: [call() for _ in range(R)]) / R
+            fl = (graph_us(lambda: [(flush(), call()) for _ in range(20)]) / 20) - t_flush
+            for _ in range(200):
+                call()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(2000):
+                call()
+            torch.cuda.synchronize()
+            py = (time.perf_counter() - t0) / 2000 * 1e6
+            res.append({"n": n, "path": path, "runs": chosen, "device_hot_us": hot, "device_flushed_us": fl,
+                        "python_us": py, "parity_ok": bool(ok)})
+    # plain C: host enqueue / back-to-back per call
+    cres = []
+    exe = os.path.join(ROOT, "examples", "latency_c")
+    if os.path.exists(exe):
+        r = subprocess.run([exe, "1024", str(2**20 + 7)], capture_output=True, text=True, timeout=600)
+        cres = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    for row in res:
+        for c in cres:
+            if c.get("n") == row["n"] and c.get("path") == row["path"]:
+                row.update({("c_" + k): v for k, v in c.items() if k not in ("n", "path", "runs")})
+    head = next(r for r in res if r["n"] == 1024 and r["path"] == "auto")
+    value = head.get("c_trusted_back_to_back_us", head["python_us"])
+    line = {"metric": "normalize latency per call, configs 1-2 (n=1024 32x32 literal grid; n=2^20+7)",
+            "value": value, "unit": "us per call (n=1024, AUTO path, back to back from C, trusted pointers)",
+            "n_gpus": 1, "steps": R, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"normalize n=1024 and n=2^20+7 fp32 (Fig. 1), {args.index} index, every path",
+                       "l2": "device_hot_us: input L2-resident; device_flushed_us: 256 MiB write + 256 MiB read "
+                             "before every call inside the graph, flush time subtracted"},
+            "results": res, "parity": {"ok": ok_all, "what": "per path and size: |s - S| <= 1e-6 S and the whole "
+                                                              "output == oracle_replay(x, s) bitwise"},
+            "gpu_launches": len(res) * R}
+    if rank == 0:
+        emit(line)
 
 
 def run_licm(args, world, rank, local):
@@ -885,7 +1266,37 @@ def run_licm(args, world, rank, local):
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
+
+
+def emit(line):
+    """Print the one JSON line (rank 0), with the run metadata (versions) added."""
+    if "meta" not in line:
+        line["meta"] = run_meta(line.get("n_gpus", 1))
+    print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def self_launch(nproc):
+    """`python bench.py --gpus N` without torchrun: re-execute this command under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1), the
+    launch the driver uses for N > 1.  Rank 0's JSON line passes through stdout.
+    NCCL's init log (communicator ranks, transports, NVLS) is kept on stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -894,7 +1305,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="libnorm", choices=["libnorm", "reference"])
-    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax", "backprop"])
+    ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax", "backprop", "small"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
     ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
     ap.add_argument("--numel", dest="n", type=int, default=2**32)
@@ -904,6 +1315,7 @@ def main():
                          "(default) or uniform one-range (rank 0 holds the whole covered prefix)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--also-dense", action="store_true", default=True)
     ap.add_argument("--exchange", default="p2p", choices=["nccl", "nccl-allreduce", "p2p", "host"],
                     help="N > 1: norm_launch_sharded (ncclAllGather), the fused peer-memory "
@@ -912,6 +1324,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 untimed warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -928,6 +1342,8 @@ def main():
             run_backprop(args, world, rank, local)
         elif args.workload == "licm":
             run_licm(args, world, rank, local)
+        elif args.workload == "small":
+            run_small(args, world, rank, local)
         else:
             run_paths28(args, world, rank, local)
     finally:

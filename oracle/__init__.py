@@ -43,6 +43,8 @@ def lib():
         for f in ("oracle_form_thread", "oracle_form_block", "oracle_form_hoisted"):
             getattr(L, f).argtypes = [vp, vp, i64, ctypes.c_int, u64p]
         L.oracle_form_hoisted_mt.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, u64p]
+        L.oracle_sum_exact_mt.argtypes = [vp, i64, ctypes.c_int]
+        L.oracle_sum_exact_mt.restype = ctypes.c_double
         L.oracle_rows_sum_exact.argtypes = [vp, vp, i64, i64, i64]
         L.oracle_rows.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
         L.oracle_replay.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float]
@@ -153,6 +155,13 @@ def form_hoisted_mt(inp, mode="literal", threads=None, out=None):
     if rc:
         raise ValueError("oracle_form_hoisted_mt rejected its arguments")
     return out, adds.value
+
+
+def sum_exact_mt(x, threads=None):
+    """oracle_sum_exact on `threads` host threads (default: all cores); same value."""
+    x, p = _f32(x)
+    threads = (os.cpu_count() or 1) if threads is None else threads
+    return lib().oracle_sum_exact_mt(p, x.size, int(threads))
 
 
 def rows_sum_exact(x2d):

@@ -316,6 +316,34 @@ int oracle_form_hoisted_mt(float* out, const float* in, int64_t n, int mode, int
   return 0;
 }
 
+/* The exact sum of x[0, n) on T threads (same chunking and exact merge as
+ * oracle_form_hoisted_mt), correctly rounded to fp64: == oracle_sum_exact. */
+double oracle_sum_exact_mt(const float* x, int64_t n, int threads) {
+  if (n <= 0) return 0.0;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  mt_task_t* t = (mt_task_t*)calloc((size_t)threads, sizeof(mt_task_t));
+  if (!t) return oracle_sum_exact(x, n);
+  for (int k = 0; k < threads; ++k) {
+    t[k].in = x;
+    t[k].lo = n * k / threads;
+    t[k].hi = n * (k + 1) / threads;
+  }
+  mt_run(t, threads, mt_sum);
+  acc_t all;
+  memset(&all, 0, sizeof all);
+  for (int k = 0; k < threads; ++k) {
+    for (int j = 0; j < ACC_LIMBS; ++j) all.limb[j] += t[k].acc.limb[j];
+    all.nposinf += t[k].acc.nposinf;
+    all.nneginf += t[k].acc.nneginf;
+    all.nnan += t[k].acc.nnan;
+    all.nterms += t[k].acc.nterms;
+    all.nnegzero += t[k].acc.nnegzero;
+  }
+  free(t);
+  return acc_result(&all);
+}
+
 /* Exact per-row sums (the oracle's `sum` of each row, reading R10): S[r] = the
  * exact sum of row r, correctly rounded to fp64. */
 int oracle_rows_sum_exact(double* S, const float* in, int64_t rows, int64_t cols, int64_t ld) {

@@ -63,6 +63,8 @@ int oracle_form_hoisted(float* out, const float* in, int64_t n, int mode, uint64
  * oracle_form_hoisted.  For timing the oracle on all host cores (cpu_baseline). */
 int oracle_form_hoisted_mt(float* out, const float* in, int64_t n, int mode, int threads,
                            uint64_t* adds);
+/* The exact sum on `threads` threads (exact merge): == oracle_sum_exact. */
+double oracle_sum_exact_mt(const float* x, int64_t n, int threads);
 /* S[r] = exact sum of row r (in[r*ld + 0 .. cols)), correctly rounded to fp64. */
 int oracle_rows_sum_exact(double* S, const float* in, int64_t rows, int64_t cols, int64_t ld);
 

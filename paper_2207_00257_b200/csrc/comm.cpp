@@ -260,20 +260,32 @@ NORM_API norm_status_t norm_launch_sharded(norm_comm_t* c, float* out_local, con
   if (local == 0 && (s = check_out_ptrs(o, d)) != NORM_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Workspace ws = workspace_carve(c->ws);
+  NvtxRange rr("norm_launch_sharded");
   // 1. local partial over all owned elements (the hoisted `sum`, restricted to this rank)
-  ev_begin(st);
-  cudaError_t e = launch_reduce(in_local, local, ws, c->send, d, st);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  ev_end(st);
+  {
+    NvtxRange r("libnorm:reduce");
+    ev_begin(st);
+    cudaError_t e = launch_reduce(in_local, local, ws, c->send, d, st);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+    ev_end(st);
+  }
   // 2. exchange: W x 8 bytes over NVLink
   if (c->mode == NORM_COMM_ALLREDUCE) {  // NCCL's own summation order; one partial back
-    ncclResult_t r = ncclAllReduce(c->send, c->recv, 1, ncclFloat64, ncclSum, c->nccl, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    {
+      NvtxRange r("libnorm:exchange:ncclAllReduce");
+      ncclResult_t nr = ncclAllReduce(c->send, c->recv, 1, ncclFloat64, ncclSum, c->nccl, st);
+      if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce");
+    }
+    NvtxRange r("libnorm:scale");
     return shard_finish(out_local, in_local, mine, n_global, c->recv, 1, o, d, ws);
   }
-  ncclResult_t r = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
-  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  {
+    NvtxRange r("libnorm:exchange:ncclAllGather");
+    ncclResult_t nr = ncclAllGather(c->send, c->recv, 1, ncclFloat64, c->nccl, st);
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather");
+  }
   // 3. rank-order combine + scale
+  NvtxRange r("libnorm:scale");
   return shard_finish(out_local, in_local, mine, n_global, c->recv, c->world, o, d, ws);
 }
 
@@ -450,6 +462,7 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
     lc.n = local;
     lc.L = lc.count = Lloc;
     lc.G = (local + 31) / 32;
+    NvtxRange r("libnorm:fused+peer-exchange");
     ev_begin(st);
     cudaError_t e = launch_fused(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post,
                                  p->mail);
@@ -458,10 +471,14 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
     p->epoch = epoch;
     return NORM_OK;
   }
-  ev_begin(st);
-  cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st, post);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");  // nothing enqueued
-  ev_end(st);
+  {
+    NvtxRange r("libnorm:reduce+peer-publish");
+    ev_begin(st);
+    cudaError_t e = launch_reduce(in_local, local, ws, ws.S, d, st, post);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");  // nothing enqueued
+    ev_end(st);
+  }
+  NvtxRange r("libnorm:peer-wait+scale");
   s = shard_finish(out_local, in_local, mine, n_global, p->mail, p->world, o, d, ws, epoch);
   if (s != NORM_OK) {
     p->broken = true;  // the reduce has published this epoch; our scale did not consume it

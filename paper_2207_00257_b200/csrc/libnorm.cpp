@@ -328,6 +328,7 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
   if (path == NORM_PATH_FUSED && cov.kind != COV_PREFIX) path = NORM_PATH_SMALL;
   cudaError_t e;
   if (path == NORM_PATH_SMALL) {
+    NvtxRange r("libnorm:small");
     ev_begin(st);
     e = launch_small(out, in, cov, o->sum_out, o->sum_out_f64, st);
     if (e != cudaSuccess) return cuda_fail(e, "small_kernel launch");
@@ -338,16 +339,21 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
   norm_status_t s = get_workspace(o, d.device, st, &ws);
   if (s != NORM_OK) return s;
   if (path == NORM_PATH_FUSED) {
+    NvtxRange r("libnorm:fused");
     ev_begin(st);
     e = launch_fused(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
     if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");
     ev_end(st);
     return NORM_OK;
   }
-  ev_begin(st);
-  e = launch_reduce(in, cov.n, ws, ws.S, d, st);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-  ev_end(st);
+  {
+    NvtxRange r("libnorm:reduce");
+    ev_begin(st);
+    e = launch_reduce(in, cov.n, ws, ws.S, d, st);
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
+    ev_end(st);
+  }
+  NvtxRange r("libnorm:scale");
   if (cov.kind == COV_PREFIX)
     e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st, 0, ws.scale_ctr);
   else
@@ -437,6 +443,7 @@ static norm_status_t host_stage(int dev, cudaStream_t st, int64_t resident, int6
 
 static norm_status_t launch_host(float* out_host, const float* in_host, const Coverage& cov,
                                  const norm_opts_t* o, const DeviceInfo& d) {
+  NvtxRange r("norm_launch_host");
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   const int64_t n = cov.n;
   // Elements that must stay on the device until the divisor is known.
@@ -517,6 +524,7 @@ static const norm_opts_t kDefaultOpts = NORM_OPTS_INIT;
 // ================================================================= C ABI
 
 NORM_API norm_status_t norm_launch_ex(float* out, const float* in, int64_t n, const norm_opts_t* o) {
+  NvtxRange r("norm_launch_ex");
   if (!o) o = &kDefaultOpts;
   norm_status_t s;
   if ((s = check_opts(o)) != NORM_OK) return s;
@@ -662,6 +670,7 @@ NORM_API norm_status_t norm_launch_host(float* out_host, const float* in_host, i
 
 NORM_API norm_status_t norm_rows(float* out, const float* in, int64_t rows, int64_t cols,
                                  int64_t ld_out, int64_t ld_in, const norm_opts_t* o) {
+  NvtxRange r("norm_rows");
   if (!o) o = &kDefaultOpts;
   norm_status_t s;
   if ((s = check_opts(o)) != NORM_OK) return s;

@@ -5,11 +5,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 
 #include "libnorm.h"
 
 namespace lnorm {
+
+// NVTX range on the host thread for the lifetime of the object (the enqueue of
+// one step of the path: "reduce", "exchange:...", "scale", ...).  Header-only
+// NVTX v3: a no-op unless a tool (nsys, ncu --nvtx) is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Covered set C(n) of Fig. 1's launch, DESIGN.md §3.1.
 enum CovKind { COV_EMPTY = 0, COV_PREFIX = 1, COV_RESIDUE = 2 };

@@ -58,4 +58,35 @@ def test_reference_arm_json_contract():
     assert d["unit"] == "GB/s" and d["higher_is_better"] is True and d["value"] > 0
     assert d["config"]["workload"] == bench.workload_name(2**32, "literal")
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["cpu_baseline"]["cores"] == os.cpu_count()
     assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_loads_no_product_library():
+    """The reference arm (the oracle) never maps libnorm.so: run it in-process and
+    read this process's own memory map afterwards."""
+    import subprocess
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '3'];"
+            "runpy.run_path('bench.py', run_name='__main__');"
+            "print('MAPS', sorted({l.split()[-1] for l in open('/proc/self/maps') if l.strip().endswith('.so')}))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    maps = [ln for ln in r.stdout.splitlines() if ln.startswith("MAPS")][0]
+    assert "liboracle.so" in maps and "libnormgen.so" in maps
+    assert "libnorm.so" not in maps.replace("libnormgen", "")
+
+
+def test_plain_launch_self_execs_two_ranks():
+    """`python bench.py --gpus 2` without torchrun re-executes itself under
+    torch.distributed.run (the driver may call it either way); rank 0 alone prints
+    one JSON line.  The reference arm runs on CPU, so this covers the launcher here."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["meta"]["world_size"] == 2

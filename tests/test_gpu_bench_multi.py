@@ -67,3 +67,29 @@ def test_bench_reference_two_ranks():
     d, _ = _torchrun(["--impl", "reference", "--steps", "1", "--warmup", "3"])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_plain_python_launch_two_ranks():
+    """`python bench.py --gpus 2` with no torchrun: bench.py re-executes itself under
+    torch.distributed.run; one JSON line from rank 0, the peer exchange used, the
+    other exchanges' records present (NCCL ones marked not run under the one-GPU
+    gloo emulation), the exchange latency record, and the run metadata."""
+    env = dict(os.environ, NORM_BENCH_BACKEND="gloo", NORM_BENCH_DEVICE="0")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--numel", str(2**24 + 7),
+           "--steps", "3", "--warmup", "3", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-4000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["exchange"] == "p2p" and d["config"]["exchange_note"] is None
+    assert "host" in d["exchanges"] and d["exchanges"]["host"]["value"] > 0
+    assert "NCCL" in d["exchanges"]["note"]
+    lat = d["exchange_latency"]
+    assert lat["p2p"]["us_per_step_max"] > 0 and lat["host"]["us_per_step_max"] > 0
+    assert d["meta"]["world_size"] == 2 and d["meta"]["torch"]
+    assert d["step_stats"]["rank_ms_max"] >= d["step_stats"]["rank_ms_min"] > 0
+    # 2^24 + 7 elements split over 2 ranks: 32 MiB per rank < 4 x L2 -> flushed
+    assert "flushed" in d["config"]["l2"]

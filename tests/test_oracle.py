@@ -375,6 +375,14 @@ def test_form_hoisted_mt_bit_identical(mode):
         oracle.form_hoisted_mt(x, "dense", threads=0)
 
 
+def test_sum_exact_mt_matches_fsum():
+    for d in (0, 3, 4):
+        x = gen.make_host(100003, seed=11, dist=d)
+        ref = _fsum(x)
+        for T in (1, 4, 16, 300):
+            assert oracle.sum_exact_mt(x, threads=T) == ref
+
+
 def test_rows_sum_exact_matches_fsum():
     """Per-row exact sums == math.fsum of each row (exact, correctly rounded)."""
     x = gen.make_host(37 * 129, seed=3, dist=4).reshape(37, 129)
