@@ -619,7 +619,7 @@ def run_vector(args, world, rank, local):
         kpath = L.choose_path(nloc, lloc, "auto")
     else:
         kpath = "two_pass"
-    fused_step = kpath == "fused"
+    fused_step = kpath in ("fused", "mid", "cluster")
     small_step = kpath == "small"
     red_bytes = 4 * nloc + (8 * max(lloc, 0) if (fused_step or small_step) else 0)
     # in-run calibration on the same buffers: a torch copy stream
@@ -720,7 +720,10 @@ def run_vector(args, world, rank, local):
     if rank != 0:
         return
     cov_count, prefix = L.coverage(n, index)
-    kname = ("fused_kernel (reduce + grid barrier + exchange + scale: the whole step)" if fused_step else
+    kname = ("cluster_kernel (one 16-CTA cluster: reduce, DSMEM combine, scale: the whole step)"
+             if kpath == "cluster" else
+             "mid_kernel (256-bit loads, grid barrier, exchange, scale: the whole step)" if kpath == "mid" else
+             "fused_kernel (reduce + grid barrier + exchange + scale: the whole step)" if fused_step else
              "small_kernel (one CTA: sum, barrier, scale: the whole step)" if small_step else
              ("reduce_dyn_kernel (TMA-bulk reduce, dynamic deterministic tail)" if nloc >= (1 << 22)
               else "reduce_kernel") + " (the hoisted sum: 4n of the step's 4n + 8|C| bytes)")
@@ -1150,7 +1153,7 @@ def run_small(args, world, rank, local):
         out = torch.empty_like(x)
         count, prefix = L.coverage(n, args.index)
         t_flush = graph_us(lambda: [flush() for _ in range(20)]) / 20
-        for path in ("auto", "small", "two_pass", "fused"):
+        for path in ("auto", "small", "cluster", "mid", "two_pass", "fused"):
             chosen = L.choose_path(n, prefix, path)
 
             def call():
@@ -1307,7 +1310,7 @@ def main():
     ap.add_argument("--impl", default="libnorm", choices=["libnorm", "reference"])
     ap.add_argument("--workload", default="vector", choices=["vector", "rows", "paths28", "licm", "softmax", "backprop", "small"])
     ap.add_argument("--index", default="literal", choices=["literal", "dense"])
-    ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small"])
+    ap.add_argument("--path", default="auto", choices=["auto", "two_pass", "fused", "small", "mid", "cluster"])
     ap.add_argument("--numel", dest="n", type=int, default=2**32)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--plan", default="balanced", choices=["balanced", "uniform"],

@@ -75,11 +75,15 @@ typedef enum {
 } norm_index_t;
 
 typedef enum {
-  NORM_PATH_AUTO = 0,     /* n <= 2^17: small; input > L2 but covered prefix fits: fused;
-                             else two-pass                                 */
+  NORM_PATH_AUTO = 0,     /* small n: small; L2-sized: mid; input > L2 but covered prefix
+                             fits: fused; else two-pass                    */
   NORM_PATH_TWO_PASS = 1, /* reduce kernel, then scale kernel (PDL-chained)               */
   NORM_PATH_FUSED = 2,    /* one cooperative kernel: reduce, grid barrier, scale from L2  */
-  NORM_PATH_SMALL = 3     /* one CTA does everything (any n; intended for n <= 2^17)       */
+  NORM_PATH_SMALL = 3,    /* one CTA does everything (any n; intended for n <= 2^17)       */
+  NORM_PATH_MID = 4,      /* one cooperative kernel of 256-bit-load CTAs, one per SM:
+                             reduce, grid barrier, scale (L2-sized inputs)                 */
+  NORM_PATH_CLUSTER = 5   /* one thread-block cluster (16 CTAs): reduce, DSMEM combine,
+                             scale -- no workspace (L2-sized inputs, e.g. 2^20 + 7)        */
 } norm_path_t;
 
 /* Options of every device entry point.  `index` and `path` carry norm_index_t /

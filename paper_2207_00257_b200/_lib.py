@@ -8,7 +8,7 @@ _DIR = os.path.dirname(os.path.abspath(__file__))
 _SO = os.environ.get("LIBNORM_SO") or os.path.join(_DIR, "libnorm.so")
 
 INDEX = {"literal": 0, "dense": 1}
-PATH = {"auto": 0, "two_pass": 1, "fused": 2, "small": 3}
+PATH = {"auto": 0, "two_pass": 1, "fused": 2, "small": 3, "mid": 4, "cluster": 5}
 STATUS = ["NORM_OK", "NORM_ERR_INVALID_VALUE", "NORM_ERR_OVERLAP", "NORM_ERR_CUDA",
           "NORM_ERR_NCCL", "NORM_ERR_WORKSPACE", "NORM_ERR_UNSUPPORTED"]
 

@@ -456,17 +456,20 @@ NORM_API norm_status_t norm_launch_sharded_peer(norm_peer_t* p, float* out_local
   const int64_t Lloc = local_covered_prefix(mine, gcov);
   int path = o->path;
   if (path == NORM_PATH_AUTO) path = auto_path(local, Lloc, Lloc >= 0, d);
-  if (path == NORM_PATH_FUSED && Lloc >= 0 && local > 0) {
+  if (path == NORM_PATH_CLUSTER || path == NORM_PATH_SMALL) path = NORM_PATH_MID;  // need the mailbox step
+  if ((path == NORM_PATH_FUSED || path == NORM_PATH_MID) && Lloc >= 0 && local > 0) {
     Coverage lc{};
     lc.kind = COV_PREFIX;
     lc.n = local;
     lc.L = lc.count = Lloc;
     lc.G = (local + 31) / 32;
-    NvtxRange r("libnorm:fused+peer-exchange");
+    NvtxRange r(path == NORM_PATH_MID ? "libnorm:mid+peer-exchange" : "libnorm:fused+peer-exchange");
     ev_begin(st);
-    cudaError_t e = launch_fused(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post,
-                                 p->mail);
-    if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");  // nothing enqueued
+    cudaError_t e = path == NORM_PATH_MID
+                        ? launch_mid(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post, p->mail)
+                        : launch_fused(out_local, in_local, lc, ws, o->sum_out, o->sum_out_f64, d, st, post,
+                                       p->mail);
+    if (e != cudaSuccess) return cuda_fail(e, "fused / mid kernel cooperative launch");  // nothing enqueued
     ev_end(st);
     p->epoch = epoch;
     return NORM_OK;

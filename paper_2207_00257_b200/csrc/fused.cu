@@ -108,6 +108,81 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   FUSED_STAMP(4)
 }
 
+// ------------------------------------------------------------------ mid
+// One launch for L2-sized inputs (configs 2: n = 2^20 + 7): the two-pass path
+// pays two launches (~8 us of host enqueue per call on this box, more than
+// the ~6 us of device time) and the TMA fused kernel's ring set-up and dynamic
+// tail cost more than they save when the whole input is a few MiB.  One
+// cooperative CTA per SM: every thread sums its 256-bit vectors of `in`
+// (coherent loads: out may alias in) with the fixed per-thread order of
+// accumulate_segment; block_sum -> partials[cta]; grid barrier (the arrival
+// count shared with fused_kernel: both grids are the SM count, so the count
+// stays a multiple of it between kernels); every CTA adds the partials in
+// index order (identical S everywhere); then the covered prefix is scaled from
+// L2.  Multi-GPU (post.mail): CTA 0 publishes the rank partial, every CTA waits
+// on the local mailbox, as in fused_kernel.
+constexpr int MID_THREADS = 512, MID_UNROLL = 2;
+template <bool VEC>
+__global__ void __launch_bounds__(MID_THREADS, 1)
+    mid_kernel(float* out, const float* in, int64_t n, int64_t L, double* partials, float* sum_out,
+               double* sum_out_f64, PeerPost post, const double* mailbox, unsigned long long* arrivals) {
+  __shared__ double red[MID_THREADS / 32];
+  __shared__ double S_sh;
+  pdl_wait();  // programmatic dependent of the preceding kernel (pdl_chain): wait for it first
+  pdl_launch_dependents();
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) target = (ld_acquire_u64(arrivals) / gridDim.x + 1) * gridDim.x;
+  double acc = 0.0;
+  accumulate_segment<MID_THREADS, MID_UNROLL, LD_PLAIN>(in, n, blockIdx.x, gridDim.x, acc, 0);
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  grid_barrier_count(arrivals, target);  // all of `in` has been read: `out` (possibly == in) may be written
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += MID_THREADS) v += __ldcg(partials + i);
+  double S = block_sum(v, red);  // identical bits in every CTA
+  if (post.mail) {
+    if (threadIdx.x == 0) {
+      if (blockIdx.x == 0) publish_partial(post, S);
+      double Sf;
+      combine_parts(mailbox, post.world, &Sf, post.epoch);
+      S_sh = Sf;
+    }
+    __syncthreads();
+    S = S_sh;
+  }
+  const float s = (float)S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (sum_out) *sum_out = s;
+    if (sum_out_f64) *sum_out_f64 = S;
+  }
+  scale_segment<MID_THREADS, MID_UNROLL, VEC, true>(out, in, L, s, blockIdx.x, gridDim.x);
+}
+
+cudaError_t launch_mid(float* out, const float* in, const Coverage& cov, const Workspace& ws,
+                       float* sum_out, double* sum_out_f64, const DeviceInfo& d, cudaStream_t st,
+                       PeerPost post, const double* mailbox) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
+  void* fn = vec ? (void*)mid_kernel<true> : (void*)mid_kernel<false>;
+  int grid = d.sms;  // one CTA per SM (the arrival count's invariant, see mid_kernel)
+  int64_t n = cov.n, L = cov.L;
+  double* partials = ws.partials;
+  unsigned long long* arrivals = ws.arrivals;
+  void* args[] = {&out, (void*)&in, &n, &L, &partials, &sum_out, &sum_out_f64, &post, (void*)&mailbox,
+                  &arrivals};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(MID_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_chain() ? 2 : 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 #ifdef NORM_TIMELINE
 extern "C" __attribute__((visibility("default"))) int norm_debug_fused_timeline(unsigned long long* host,
                                                                                  int n) {

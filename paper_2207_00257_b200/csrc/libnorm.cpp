@@ -228,7 +228,7 @@ static bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3
 norm_status_t check_opts(const norm_opts_t* o) {
   if (o->index != NORM_INDEX_LITERAL && o->index != NORM_INDEX_DENSE)
     return fail(NORM_ERR_INVALID_VALUE, "bad index mode");
-  if (o->path < NORM_PATH_AUTO || o->path > NORM_PATH_SMALL)
+  if (o->path < NORM_PATH_AUTO || o->path > NORM_PATH_CLUSTER)
     return fail(NORM_ERR_INVALID_VALUE, "bad path");
   if ((o->flags & ~NORM_FLAG_TRUSTED_PTRS) != 0u || o->reserved != 0u)
     return fail(NORM_ERR_INVALID_VALUE, "unknown flags or nonzero reserved field");
@@ -296,23 +296,35 @@ static norm_status_t check_literal_grid(const Coverage& c, int index) {
   return NORM_OK;
 }
 
-// AUTO path thresholds, measured on B200 (scripts/small_paths.py,
+// AUTO path thresholds, measured on B200: device time per call
+// from CUDA graphs of back-to-back calls, L2 flushed before each call
+// (scripts/path_sweep.py -> profiles/round2/path_sweep*.txt; earlier
 // scripts/fused_vs_twopass.py, profiles/r05/fused_*.txt):
-//  * n <= 2^17: one CTA does everything (3-6 us; the two-kernel path costs ~6.5 us);
-//  * fused when the input does NOT fit in L2 and only part of it is covered,
-//    with the covered bytes <= 3 x L2: one kernel instead of two saves the second
-//    launch and ramp, and the prefix read last is (partly) served from L2 —
-//    literal 2^27..2^31: 6-9 us faster per call; at 2^32 (512 MiB prefix) the
-//    fused scale phase's plain loads lose to the two-pass TMA scale (+15 us).
-//    When the whole input fits in L2 the two-pass scale hits L2 anyway and the
-//    cooperative launch + grid barrier only cost (~1 us); dense stays two-pass;
-//  * otherwise two-pass.
-constexpr int64_t kSmallN = 1 << 17;
+//  * n <= 3 x 2^15: one CTA does everything (2.4-4 us; mid 4.4-4.7 us);
+//  * covered set a prefix and 4n <= 2 L2 (literal) / 0.6 L2 (dense, whose
+//    scale re-reads and writes all of it): mid, one cooperative launch of
+//    256-bit-load CTAs -- the TMA kernels' fixed cost (ring set-up, dynamic
+//    tail, second launch) dominates below that: literal 2^20+7 / 2^22 / 2^25:
+//    mid 8.0 / 9.9 / 29.5 us vs two-pass 8.5 / 14.2 / 33.2 vs fused 12.9 / 14.2 /
+//    32.8; 2^26 ties (50.5 / 51.4 / 50.9); dense 2^24: mid 30.7, fused 33.3,
+//    two-pass 41.9;
+//  * fused (TMA ring, covered prefix read last with evict_last, scaled from L2)
+//    for partial coverage with input > 2 L2 and covered bytes <= 3 L2 (literal
+//    2^27..2^31: 5-9 us faster than two-pass; at 2^32 the 512 MiB prefix
+//    streams from HBM and the two-pass TMA scale wins by 15 us), and for full
+//    coverage with 0.6 L2 < 4n <= 2 L2 (dense 2^25 / 2^26: 62.3 / 122.7 us vs
+//    two-pass 72.4 / 128.7);
+//  * otherwise two-pass (dense 2^27: 242 vs fused 245; 2^28: 469 vs 489).
+constexpr int64_t kSmallN = 3 << 15;
 
 int auto_path(int64_t n, int64_t L, bool prefix, const DeviceInfo& d) {
   if (n <= kSmallN) return NORM_PATH_SMALL;
-  if (prefix && L < n && (size_t)n * 4 > d.l2_bytes && (size_t)L * 4 <= 3 * d.l2_bytes)
-    return NORM_PATH_FUSED;
+  if (!prefix) return NORM_PATH_TWO_PASS;
+  const double bytes = 4.0 * (double)n, l2 = (double)d.l2_bytes;
+  const bool full = L >= n;
+  if (bytes <= (full ? 0.6 : 2.0) * l2) return NORM_PATH_MID;
+  if (!full && (double)L * 4.0 <= 3.0 * l2) return NORM_PATH_FUSED;
+  if (full && bytes <= 2.0 * l2) return NORM_PATH_FUSED;
   return NORM_PATH_TWO_PASS;
 }
 
@@ -325,8 +337,17 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
                                    const norm_opts_t* o, const DeviceInfo& d) {
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   int path = choose_path(cov, o, d);
-  if (path == NORM_PATH_FUSED && cov.kind != COV_PREFIX) path = NORM_PATH_SMALL;
+  if ((path == NORM_PATH_FUSED || path == NORM_PATH_MID || path == NORM_PATH_CLUSTER) && cov.kind != COV_PREFIX)
+    path = NORM_PATH_SMALL;
   cudaError_t e;
+  if (path == NORM_PATH_CLUSTER) {
+    NvtxRange r("libnorm:cluster");
+    ev_begin(st);
+    e = launch_cluster(out, in, cov, o->sum_out, o->sum_out_f64, d, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cluster_kernel launch");
+    ev_end(st);
+    return NORM_OK;
+  }
   if (path == NORM_PATH_SMALL) {
     NvtxRange r("libnorm:small");
     ev_begin(st);
@@ -343,6 +364,14 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
     ev_begin(st);
     e = launch_fused(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
     if (e != cudaSuccess) return cuda_fail(e, "fused_kernel cooperative launch");
+    ev_end(st);
+    return NORM_OK;
+  }
+  if (path == NORM_PATH_MID) {
+    NvtxRange r("libnorm:mid");
+    ev_begin(st);
+    e = launch_mid(out, in, cov, ws, o->sum_out, o->sum_out_f64, d, st);
+    if (e != cudaSuccess) return cuda_fail(e, "mid_kernel cooperative launch");
     ev_end(st);
     return NORM_OK;
   }
@@ -548,7 +577,7 @@ struct norm_graph {
 
 NORM_API norm_status_t norm_choose_path(int64_t n, int64_t covered_prefix, int32_t requested,
                                         int32_t* chosen) {
-  if (n < 0 || !chosen || requested < NORM_PATH_AUTO || requested > NORM_PATH_SMALL ||
+  if (n < 0 || !chosen || requested < NORM_PATH_AUTO || requested > NORM_PATH_CLUSTER ||
       covered_prefix > n)
     return fail(NORM_ERR_INVALID_VALUE, "bad norm_choose_path arguments");
   DeviceInfo d;

@@ -66,6 +66,7 @@ bool device_info(DeviceInfo* out, std::string* err);
 
 enum PdlMode { PDL_OFF = 0, PDL_EARLY = 1, PDL_LATE = 2 };
 int pdl_mode();  // NORM_PDL env knob, read once (reduce.cu)
+bool pdl_chain();  // NORM_PDL_CHAIN: small / mid kernels as programmatic dependents (reduce.cu)
 
 // ---- kernel launchers.  All return the launch's cudaError_t. ----
 // Tuning constants live next to the kernels.
@@ -123,6 +124,17 @@ cudaError_t launch_fused(float* out, const float* in, const Coverage& cov, const
                          float* sum_out, double* sum_out_f64, const DeviceInfo& d,
                          cudaStream_t st, PeerPost post = PeerPost{nullptr, 0, 0, 0},
                          const double* mailbox = nullptr);
+
+// One cooperative LDG.E.256 kernel (one CTA per SM): reduce, grid barrier, scale of
+// the covered prefix from L2 (NORM_PATH_MID: L2-sized inputs).  Requires COV_PREFIX.
+cudaError_t launch_mid(float* out, const float* in, const Coverage& cov, const Workspace& ws,
+                       float* sum_out, double* sum_out_f64, const DeviceInfo& d, cudaStream_t st,
+                       PeerPost post = PeerPost{nullptr, 0, 0, 0}, const double* mailbox = nullptr);
+
+// The whole call in one thread-block cluster (16 CTAs, DSMEM combine; NORM_PATH_
+// CLUSTER, cluster.cu).  Requires COV_PREFIX.  No workspace.
+cudaError_t launch_cluster(float* out, const float* in, const Coverage& cov, float* sum_out,
+                           double* sum_out_f64, const DeviceInfo& d, cudaStream_t st);
 
 // Batched rows: one CTA per row (grid-strided), row held in registers when it fits.
 // row_ctr (Workspace::row_ctr, zeroed; left zeroed) or NULL: rows dealt from a

@@ -145,6 +145,18 @@ int pdl_mode() {
   return mode;
 }
 
+// Latency-bound one-launch paths (small, mid) are launched as programmatic
+// dependents of whatever precedes them on the stream and trigger their own
+// dependents at entry, so back-to-back calls overlap one launch's latency with
+// the previous call (NORM_PDL_CHAIN=0 turns it off for A/B runs).
+bool pdl_chain() {
+  static const bool on = [] {
+    const char* e = getenv("NORM_PDL_CHAIN");
+    return !(e && !strcmp(e, "0"));
+  }();
+  return on;
+}
+
 // Dynamic tail of the bulk reduce / fused phase 1: the last pct % of the chunks
 // (NORM_DYN_PCT, default kDynPct; 0 = fully static reduce_bulk_kernel) but at
 // least kDynMinTasksPerCTA tasks per CTA, so smaller inputs still get a fine

@@ -155,6 +155,12 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(SMALL_THREADS)
     small_kernel(float* out, const float* in, int64_t n, int kind, int64_t L, int64_t G,
                  float* sum_out, double* sum_out_f64) {
+  // Launched as a programmatic dependent of whatever precedes it on the stream
+  // (back-to-back latency-bound calls: the next call's CTA is resident while
+  // this one runs): wait for the predecessor's completion and memory before
+  // touching anything, then let the next call launch.
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double red[SMALL_THREADS / 32];
   double acc = 0.0;
   accumulate_segment<SMALL_THREADS, 1, LD_PLAIN>(in, n, 0, 1, acc, 0);
@@ -221,9 +227,8 @@ cudaError_t launch_scale_residue(float* out, const float* in, int64_t len, int64
 
 cudaError_t launch_small(float* out, const float* in, const Coverage& cov, float* sum_out,
                          double* sum_out_f64, cudaStream_t st) {
-  small_kernel<<<1, SMALL_THREADS, 0, st>>>(out, in, cov.n, cov.kind, cov.L, cov.G, sum_out,
-                                            sum_out_f64);
-  return cudaGetLastError();
+  return launch_maybe_pdl(small_kernel, 1, SMALL_THREADS, pdl_chain(), st, out, in, cov.n, (int)cov.kind,
+                          cov.L, cov.G, sum_out, sum_out_f64);
 }
 
 }  // namespace lnorm

@@ -33,8 +33,8 @@ def test_vector_fuzz():
     for case in range(120):
         n = max(0, _len(rng))
         mode = rng.choice(["literal", "dense"])
-        path = rng.choice(["auto", "auto", "two_pass", "fused", "small"]) if n <= 2**20 else \
-            rng.choice(["auto", "two_pass", "fused"])
+        path = rng.choice(["auto", "auto", "two_pass", "fused", "small", "mid", "cluster"]) if n <= 2**20 else \
+            rng.choice(["auto", "two_pass", "fused", "mid", "cluster"])
         dist = rng.randrange(5)
         off_in, off_out = rng.randrange(8), rng.randrange(8)
         in_place = rng.random() < 0.2

@@ -18,7 +18,7 @@ import paper_2207_00257_b200 as L
 pytestmark = pytest.mark.gpu
 
 SENTINEL_BITS = 0x7FC0FFEE  # a quiet NaN payload no kernel produces
-PATHS = ["auto", "two_pass", "fused", "small"]
+PATHS = ["auto", "two_pass", "fused", "small", "mid", "cluster"]
 DISTS = [0, 1, 2, 3, 4]
 
 
@@ -159,7 +159,7 @@ def test_special_values():
         "cancel": np.concatenate([np.full(2048, 1.0), np.full(2048, -1.0), [2.0**-20]]).astype(np.float32),
     }
     for name, x in cases.items():
-        for path in ("two_pass", "fused", "small"):
+        for path in ("two_pass", "fused", "small", "mid", "cluster"):
             out, s, _ = run(x, "dense", path)
             S = oracle.sum_exact(x)
             if math.isnan(S):
@@ -541,7 +541,7 @@ def test_signed_zeros_and_zero_heavy():
             if sign < 0:
                 xs[m] = -xs[m]  # keep a mix of +0 / -0 either way
             for mode in ("literal", "dense"):
-                for path in ("two_pass", "fused", "small"):
+                for path in ("two_pass", "fused", "small", "mid", "cluster"):
                     out, s, _ = run(xs, mode, path)
                     rep = oracle.replay(xs, s, mode, out=sentinel(n))
                     assert out.view(np.uint32).tobytes() == rep.view(np.uint32).tobytes()
@@ -640,7 +640,9 @@ def test_host_entry_pageable():
 
 @pytest.mark.parametrize("n,mode,path", [(1000, "literal", "auto"), (2**20 + 7, "literal", "auto"),
                                          (3 * 2**20 + 5, "dense", "two_pass"),
-                                         (2**22 + 9, "dense", "fused"), (2**23 + 1, "literal", "auto")])
+                                         (2**22 + 9, "dense", "fused"), (2**23 + 1, "literal", "auto"),
+                                         (2**20 + 7, "literal", "mid"), (2**21 + 3, "dense", "mid"),
+                                         (2**20 + 7, "literal", "cluster"), (2**21 + 3, "dense", "cluster")])
 def test_graph_plan_matches_eager(n, mode, path):
     x = to_dev(gen.make_host(n, seed=n % 101, dist=0))
     ref = to_dev(sentinel(n))
@@ -648,7 +650,7 @@ def test_graph_plan_matches_eager(n, mode, path):
     s = torch.zeros(1, device="cuda")
     L.normalize(ref, x, index=mode, path=path)
     g = L.NormGraph(out, x, index=mode, path=path, sum_out=s)
-    for _ in range(3 if path != "fused" else 25):  # fused: the grid barrier's arrival count keeps growing
+    for _ in range(3 if path not in ("fused", "mid") else 25):  # grid barrier's arrival count keeps growing
         g.launch()
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
@@ -691,7 +693,8 @@ def test_auto_fused_literal_mid_sizes(n):
     assert torch.equal(s, s2) and torch.equal(out[:prefix], out2[:prefix])
 
 
-@pytest.mark.parametrize("offset,path", [(0, "two_pass"), (3, "two_pass"), (0, "fused"), (5, "fused")])
+@pytest.mark.parametrize("offset,path", [(0, "two_pass"), (3, "two_pass"), (0, "fused"), (5, "fused"),
+                                         (0, "mid"), (5, "mid"), (0, "cluster"), (3, "cluster")])
 def test_dynamic_tail_deterministic(offset, path):
     """The bulk reduce hands its last chunks out dynamically (whichever CTA runs
     dry first takes the next task); the sum must not depend on who ran what.
