@@ -13,7 +13,6 @@ CHDR    := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/libnorm.h
 all: oracle/liboracle.so gen/libnormgen.so gen/libnormgen_cuda.so $(PKG)/libnorm.so
 # Oracle: plain C, no contraction, no fast-math (threads only in the cpu_baseline timer
 # oracle_form_hoisted_mt, bit-identical to form 3); shares nothing with the CUDA path.
-# Oracle: plain C, no contraction, no fast-math, no threads; shares nothing with the CUDA path.
 oracle/liboracle.so: oracle/norm_oracle.c oracle/norm_oracle.h
 	$(CC) -std=c11 -O2 -ffp-contract=off -fno-fast-math -pthread -fPIC -shared -o $@ $< -lm -lpthread
 
@@ -51,7 +50,8 @@ $(PKG)/faults/libnorm_fault%.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DNORM_FAULT=$* -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib 2> /dev/null
 
-# Timeline probe build (scripts/fused_timeline.py only; never loaded by the product)
+# Timeline probe build (scripts/fused_timeline.py, scripts/pdl_timeline.py only; never
+# loaded by the product)
 $(PKG)/faults/libnorm_timeline.so: $(CSRC) $(CHDR)
 	@mkdir -p $(PKG)/faults
 	$(NVCC) $(NVFLAGS) -DNORM_TIMELINE -shared -o $@ $(CSRC) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \

@@ -41,16 +41,53 @@ def load_peak():
         return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
+# Source files that define each workload's dominant kernel: a committed ncu
+# traffic figure counts only while their SHA-256 equals the one recorded at capture.
+_CS = "paper_2207_00257_b200/csrc/"
+_COMMON = [_CS + "device_common.cuh", _CS + "stream_common.cuh", _CS + "norm_internal.h"]
+TRAFFIC_SOURCES = {
+    "vector": [_CS + "reduce.cu"] + _COMMON,
+    "scale": [_CS + "scale.cu"] + _COMMON,
+    "paths28": [_CS + "fused.cu"] + _COMMON,
+    "rows": [_CS + "rows.cu"] + _COMMON,
+    "softmax": [_CS + "rowops.cu", _CS + "device_common.cuh", _CS + "norm_internal.h"],
+    "backprop": [_CS + "backprop.cu"] + _COMMON,
+    "small": [_CS + "fused.cu", _CS + "scale.cu"] + _COMMON,
+}
+
+
+def sources_sha256(files):
+    import hashlib
+    h = hashlib.sha256()
+    for f in files:
+        with open(os.path.join(ROOT, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()
+
+
 def load_traffic(workload, index):
-    """dram__bytes_read.sum + dram__bytes_write.sum per reduce launch, from the
-    committed ncu --set full summary (profiles/), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the workload's
+    dominant kernel, from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic_update.py), or None
+    when there is no capture or the kernel's sources changed since it was taken."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(f"{workload}:{index}")
+            e = json.load(f).get(f"{workload}:{index}")
+        if not isinstance(e, dict) or e.get("sources_sha256") != sources_sha256(e["sources"]):
+            return None
+        return e["bytes"]
     except Exception:
         return None
+
+
+def single_kernel_roofline(algo_bytes, ms, peak, peak_src, kernel, traffic):
+    """roofline object for a workload whose step is ONE kernel launch (the
+    dominant kernel is the whole step): achieved = algorithmic bytes / launch time."""
+    a = algo_bytes / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+            "traffic": traffic, "kernel": kernel, "algorithmic_bytes_per_launch": algo_bytes,
+            "avg_launch_ms": ms, "share_of_step": 1.0, "peak_source": peak_src}
 
 
 class ClockSampler:
@@ -962,7 +999,12 @@ def run_paths28(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"normalize n=2^28 fp32, {args.index}, best path = {best}",
                        "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
-            "paths": res, "peak": peak, "gpu_launches": args.steps}
+            "paths": res, "peak": peak, "gpu_launches": args.steps * 3}  # two-pass (2 kernels) + fused (1) per step
+    if best == "fused":
+        line["roofline"] = single_kernel_roofline(
+            L.algorithmic_bytes(n, args.index), res["fused"]["ms_per_step"], peak, src,
+            "fused_kernel (single pass, grid barrier; scored on 4n + 8|C|)",
+            load_traffic("paths28", args.index))
     if rank == 0:
         emit(line)
 
@@ -1042,6 +1084,9 @@ def run_softmax(args, world, rank, local):
             "config": {"workload": "norm_softmax_rows 65536x4096 fp32 (D3 signed logits)",
                        "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "frac_of_hbm_peak": res["softmax"]["frac"], "peak": peak, "results": res,
+            "roofline": single_kernel_roofline(8 * R * C, res["softmax"]["ms_per_step"], peak, src,
+                                               "softmax_vec_kernel (one read + one write per element)",
+                                               load_traffic("softmax", "dense")),
             "gpu_launches": args.steps}
     if rank == 0:
         emit(line)
@@ -1079,7 +1124,7 @@ def run_backprop(args, world, rank, local):
             times.append(a.elapsed_time(b))
         ms = sum(times) / len(times)
         res[v] = {"ms_per_step": ms, "value": nbytes / (ms / 1e3) / 1e9}
-    peak, _ = load_peak()
+    peak, peak_src = load_peak()
     line = {"metric": "bpnn_layerforward GB/s (Rodinia backprop, Fig. backprop), in=2^22, hid=16",
             "value": res["tma"]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["tma"]["ms_per_step"],
@@ -1087,6 +1132,9 @@ def run_backprop(args, world, rank, local):
             "data": "synthetic", "config": {"workload": "norm_bpnn_layerforward in=2^22 hid=16",
                                             "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
             "variants": res, "frac_of_hbm_peak": res["tma"]["value"] / peak,
+            "roofline": single_kernel_roofline(nbytes, res["tma"]["ms_per_step"], peak, peak_src,
+                                               "bpnn_tma_kernel (hidden read + write, input read, output write)",
+                                               load_traffic("backprop", "tma")),
             "speedup_eliminated_over_printed": res["printed"]["ms_per_step"] / res["eliminated"]["ms_per_step"],
             "speedup_register_over_printed": res["printed"]["ms_per_step"] / res["register"]["ms_per_step"],
             "speedup_tma_over_printed": res["printed"]["ms_per_step"] / res["tma"]["ms_per_step"],

@@ -82,6 +82,18 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
 }
 
+#ifdef NORM_TIMELINE  // probe builds only (scripts/pdl_timeline.py): per-CTA %globaltimer stamps
+__device__ unsigned long long g_reduce_ts[4096 * 4];
+#define RED_STAMP(k) \
+  if (threadIdx.x == 0) g_reduce_ts[blockIdx.x * 4 + (k)] = globaltimer_ns();
+extern "C" __attribute__((visibility("default"))) int norm_debug_reduce_timeline(unsigned long long* host,
+                                                                                  int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_reduce_ts, (size_t)n * sizeof(unsigned long long));
+}
+#else
+#define RED_STAMP(k)
+#endif
+
 // Pass 1, TMA-bulk with a dynamically scheduled, still deterministic tail
 // (dyn_stream_sum, stream_common.cuh): per-CTA partials for the grid-strided
 // chunks, task sums for the last `dyn` chunks; the last CTA adds the partials,
@@ -91,6 +103,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
                       unsigned* __restrict__ ticket, double* __restrict__ S_out, int early_trigger,
                       PeerPost post, unsigned* __restrict__ task_ctr, double* __restrict__ task_sums,
                       int64_t dyn, int tc) {
+  RED_STAMP(0);  // entry
   if (early_trigger) pdl_launch_dependents();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[BK_STAGES], empty[BK_STAGES];
@@ -102,6 +115,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   const DynSeg seg[1] = {{in, n, 0, 0}};
   int64_t ntasks;
   const double acc = dyn_stream_sum<1>(r, seg, dyn, tc, task_ctr, task_sums, dsm, &ntasks);
+  RED_STAMP(1);  // streaming done (the late PDL trigger)
   if (!early_trigger) pdl_launch_dependents();
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
@@ -110,6 +124,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
   }
   __syncthreads();
+  RED_STAMP(2);  // partial published
   if (!is_last) return;
   __threadfence();
   double v = 0.0;
@@ -122,6 +137,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     *task_ctr = 0u;
     publish_partial(post, S);
   }
+  RED_STAMP(3);  // last CTA: S written
 }
 
 int reduce_grid(const DeviceInfo& d, int64_t n) {

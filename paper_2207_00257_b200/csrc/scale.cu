@@ -10,6 +10,17 @@
 
 namespace lnorm {
 
+#ifdef NORM_TIMELINE  // probe builds only (scripts/pdl_timeline.py): per-CTA %globaltimer stamps
+__device__ unsigned long long g_scale_ts[4096 * 5];
+#define SCL_STAMP(k) g_scale_ts[blockIdx.x * 5 + (k)] = globaltimer_ns();
+extern "C" __attribute__((visibility("default"))) int norm_debug_scale_timeline(unsigned long long* host,
+                                                                                 int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_scale_ts, (size_t)n * sizeof(unsigned long long));
+}
+#else
+#define SCL_STAMP(k)
+#endif
+
 // ---------------------------------------------------------------- scale
 template <bool VEC, bool ALIAS>
 __global__ void __launch_bounds__(SC_THREADS)
@@ -55,6 +66,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   constexpr int64_t CF = SB_CHUNK / 4;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
+      SCL_STAMP(0);  // producer entry (before griddepcontrol.wait: PDL lets it start early)
       if (!ctr) {
         bulk_produce<false>(r, in, len, 0);
       } else {
@@ -70,6 +82,9 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
           stage_chunk[r.stage] = c;
           mbar_arrive_expect_tx(&r.full[r.stage], SB_CHUNK);
           bulk_g2s(r.buf + (size_t)r.stage * SB_CHUNK, body + c * CF, SB_CHUNK, &r.full[r.stage]);
+#ifdef NORM_TIMELINE
+          if (r.issued == 0) SCL_STAMP(1);  // first TMA chunk issued
+#endif
           ++r.issued;
           r.advance();
         }
@@ -89,6 +104,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   const int ct = threadIdx.x - 32;
   pdl_wait();
   if (ct == 0) {
+    SCL_STAMP(2);  // griddepcontrol.wait returned: the reduce grid is complete
     double S;
     const float s = combine_parts(S_parts, nparts, &S, epoch);
     s_sh = s;
@@ -99,6 +115,9 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
   const Divisor dv = make_divisor(s_sh);
+#ifdef NORM_TIMELINE
+  bool first = true;
+#endif
   if (!ctr) {
     bulk_scale_consume(r, out, in, len, dv, ct);
     return;
@@ -118,9 +137,16 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
       const float4 a = q[2 * i], b = q[2 * i + 1];
       st8_stream(oc + (int64_t)i * 8, div8_fchk(f8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}}, dv));
     }
+#ifdef NORM_TIMELINE
+    if (first && ct == 0) SCL_STAMP(3);  // first chunk divided and stored
+    first = false;
+#endif
     stage_release(&r.empty[r.stage]);
     r.advance();
   }
+#ifdef NORM_TIMELINE
+  if (ct == 0) SCL_STAMP(4);  // last chunk stored
+#endif
   const int64_t rbeg = head + nchunks * CF;  // remainder, then the head
   for (int64_t i = rbeg + (int64_t)blockIdx.x * BK_CONSUMERS + ct; i < len;
        i += (int64_t)gridDim.x * BK_CONSUMERS)

@@ -90,3 +90,25 @@ def test_plain_launch_self_execs_two_ranks():
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["meta"]["world_size"] == 2
+
+
+def test_traffic_bound_to_kernel_sources(tmp_path, monkeypatch):
+    """roofline.traffic is reported only while the kernel sources hash to the value
+    recorded at ncu capture time; any edit to them makes it null (stale)."""
+    import json
+    import shutil
+    root = tmp_path / "r"
+    for f in set(sum(bench.TRAFFIC_SOURCES.values(), [])):
+        (root / os.path.dirname(f)).mkdir(parents=True, exist_ok=True)
+        shutil.copy(os.path.join(ROOT, f), root / f)
+    (root / "profiles").mkdir()
+    src = bench.TRAFFIC_SOURCES["vector"]
+    monkeypatch.setattr(bench, "ROOT", str(root))
+    e = {"bytes": 123, "sources": src, "sources_sha256": bench.sources_sha256(src)}
+    (root / "profiles" / "ncu_traffic.json").write_text(json.dumps({"vector:literal": e, "rows:dense": 7}))
+    assert bench.load_traffic("vector", "literal") == 123
+    assert bench.load_traffic("rows", "dense") is None       # no hash: not trusted
+    assert bench.load_traffic("softmax", "dense") is None    # no capture
+    with open(root / src[0], "a") as f:
+        f.write("\n// edited\n")
+    assert bench.load_traffic("vector", "literal") is None   # source changed since capture
