@@ -12,5 +12,6 @@ done
 python bench.py --workload softmax > $OUT/bench_${TAG}_softmax.json 2>/dev/null
 python bench.py --workload licm > $OUT/bench_${TAG}_licm.json 2>/dev/null
 python bench.py --workload backprop > $OUT/bench_${TAG}_backprop.json 2>/dev/null
+python bench.py --workload small > $OUT/bench_${TAG}_small.json 2>/dev/null
 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_${TAG}_reference.json 2>/dev/null
 for f in $OUT/bench_${TAG}_*.json; do echo "$f: $(head -c 300 $f)"; done
