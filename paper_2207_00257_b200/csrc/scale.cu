@@ -154,6 +154,52 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   if (blockIdx.x == 0 && ct < head) out[ct] = div_rn(in[ct], dv);
 }
 
+// Scale, one-tile-per-CTA variant (the default for out/in co-aligned mod 32 B):
+// a NON-persistent grid of (len - head) / TILE_F CTAs, each loading one
+// contiguous TILE_F-float tile with 256-bit loads (one per thread) BEFORE
+// griddepcontrol.wait -- `in` is not written by the preceding reduce -- then
+// reading s, dividing and storing.  The hardware block scheduler hands tiles out
+// in index order as CTAs retire, so the reads and writes of the whole GPU sweep
+// the buffers as one contiguous wavefront; this measured 6.99 TB/s (n = 2^32,
+// IEEE division) against 6.69-6.78 for the persistent TMA ring above and 5.8-6.0
+// for persistent grid-stride loops of the same loads
+// (scripts/microbench_scale2.cu, profiles/round2/mb_scale2_*.txt).  CTA index
+// `ntiles` (the grid's last) takes the unaligned head and the ragged remainder.
+// ALIAS (out == in): coherent loads instead of the read-only path; each element
+// is read and written by the same thread, so aliasing needs nothing else.
+constexpr int TILE_THREADS = 256;
+constexpr int64_t TILE_F = (int64_t)TILE_THREADS * 8;
+template <bool ALIAS>
+__global__ void __launch_bounds__(TILE_THREADS)
+    scale_tile_kernel(float* out, const float* in, int64_t len, int64_t head, int64_t ntiles,
+                      const double* __restrict__ S_parts, int nparts, float* sum_out, double* sum_out_f64,
+                      unsigned long long epoch) {
+  __shared__ float s_sh;
+  const bool body = (int64_t)blockIdx.x < ntiles;
+  const int64_t off = head + (int64_t)blockIdx.x * TILE_F + (int64_t)threadIdx.x * 8;
+  f8 v;
+  if (body) v = ALIAS ? ld8(in + off) : ld8_stream(in + off);
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    double S;
+    const float s = combine_parts(S_parts, nparts, &S, epoch);
+    s_sh = s;
+    if (blockIdx.x == 0) {
+      if (sum_out) *sum_out = s;
+      if (sum_out_f64) *sum_out_f64 = S;
+    }
+  }
+  __syncthreads();
+  const Divisor dv = make_divisor(s_sh);
+  if (body) {
+    st8_stream(out + off, div8_fchk(v, dv));
+    return;
+  }
+  for (int64_t i = threadIdx.x; i < head; i += TILE_THREADS) out[i] = div_rn(in[i], dv);
+  for (int64_t i = head + ntiles * TILE_F + threadIdx.x; i < len; i += TILE_THREADS)
+    out[i] = div_rn(in[i], dv);
+}
+
 __global__ void __launch_bounds__(256)
     scale_residue_kernel(float* out, const float* in, int64_t len, int64_t gbegin, int64_t G,
                          const double* __restrict__ S_parts, int nparts, float* sum_out,
@@ -214,7 +260,26 @@ cudaError_t launch_scale(float* out, const float* in, int64_t len, const double*
   if (g < 1) g = 1;
   const bool vec = ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 31u) == 0;
   const bool alias = out == in;
-  if (vec && len >= kBulkMinN) {
+  // NORM_SCALE_KERNEL=tile (default) | bulk | grid: which co-aligned scale kernel
+  // (A/B runs only; every choice gives the same bits).
+  static const int which = [] {
+    const char* e = getenv("NORM_SCALE_KERNEL");
+    if (e && !strcmp(e, "bulk")) return 1;
+    if (e && !strcmp(e, "grid")) return 2;
+    return 0;
+  }();
+  if (vec && which == 0) {
+    int64_t head = (int64_t)(((32u - (reinterpret_cast<uintptr_t>(in) & 31u)) & 31u) / 4u);
+    if (head > len) head = len;
+    const int64_t ntiles = (len - head) / TILE_F;
+    if (ntiles + 1 > 0x7fffffffll) return cudaErrorInvalidConfiguration;
+    if (alias)
+      return launch_maybe_pdl(scale_tile_kernel<true>, (int)(ntiles + 1), TILE_THREADS, pdl, st, out, in,
+                              len, head, ntiles, S_parts, nparts, sum_out, sum_out_f64, epoch);
+    return launch_maybe_pdl(scale_tile_kernel<false>, (int)(ntiles + 1), TILE_THREADS, pdl, st, out, in,
+                            len, head, ntiles, S_parts, nparts, sum_out, sum_out_f64, epoch);
+  }
+  if (vec && len >= kBulkMinN && which == 1) {
     static int configured[64] = {0};
     if (d.device < 64 && !configured[d.device]) {
       cudaError_t e = cudaFuncSetAttribute(scale_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
