@@ -606,21 +606,42 @@ def run_vector(args, world, rank, local):
         # the fused peer-memory exchange, cross-checked once against the gathered
         # partials (same kernels, exchange over the process group); any failure or
         # mismatch falls back to NCCL and is recorded in the JSON line
+        # Every rank runs the same sequence of collectives whatever fails locally
+        # (PeerComm agrees on set-up failures itself; the check below is one MIN
+        # all-reduce), so a failure on one rank cannot leave the others waiting
+        # in a collective the failed rank never enters.
+        import torch.distributed as dist
+        err = None
         try:
             comm = L.PeerComm()
+        except Exception as e:  # noqa: BLE001  (raised on every rank together)
+            err = str(e)
+        if comm is not None:
             s_p = torch.zeros(1, device="cuda")
             s_g = torch.zeros(1, device="cuda")
-            comm.normalize_sharded(out, inp, mine, n, index=index, sum_out=s_p)
-            L.normalize_sharded_via(out, inp, mine, n, host_all_gather(world), index=index, sum_out=s_g)
-            torch.cuda.synchronize()
-            ok = torch.tensor([1.0 if torch.equal(s_p, s_g) else 0.0], device=_dev() if _dev() == "cuda" else "cpu")
-            import torch.distributed as dist
+            try:
+                comm.normalize_sharded(out, inp, mine, n, index=index, sum_out=s_p)
+            except Exception as e:  # noqa: BLE001
+                err = f"norm_launch_sharded_peer: {e}"
+            try:
+                L.normalize_sharded_via(out, inp, mine, n, host_all_gather(world), index=index, sum_out=s_g)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001
+                err = err or f"gathered cross-check: {e}"
+            if err is None and not torch.equal(s_p, s_g):
+                err = "p2p divisor != gathered divisor"
+            ok = torch.tensor([1.0 if err is None else 0.0], device=_dev() if _dev() == "cuda" else "cpu")
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() != 1.0:
-                raise RuntimeError("p2p divisor != gathered divisor")
-        except Exception as e:  # noqa: BLE001
-            exchange_note = f"p2p unavailable ({e}); fell back to nccl"
+                err = err or "another rank's peer exchange failed"
+        if err is not None:
+            exchange_note = f"p2p unavailable ({err}); fell back to nccl"
             print(f"[bench] {exchange_note}", file=sys.stderr)
+            if comm is not None:
+                try:
+                    comm.destroy()
+                except Exception:  # noqa: BLE001
+                    pass
             comm = None
             args.exchange = "nccl"
     if world > 1 and args.exchange in ("nccl", "nccl-allreduce") and comm is None:
