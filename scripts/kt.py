@@ -1,0 +1,60 @@
+"""Kernel timer for same-box A/B probes (with scripts/ab_libs.py or ab_env.sh):
+the row and fused workloads, K back-to-back calls between CUDA events, median
+of R such groups, one line per workload (µs per call).  Much lighter than
+bench.py (no parity, e2e or CPU legs).  KT_WORK selects workloads
+(comma-separated: softmax, rows_dense, rows_literal, fused28, dense28, backprop)."""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import gen
+import paper_2207_00257_b200 as L
+
+WORK = os.environ.get("KT_WORK", "softmax,rows_dense,rows_literal,fused28,dense28,backprop").split(",")
+K, R = int(os.environ.get("KT_K", "20")), int(os.environ.get("KT_R", "7"))
+
+
+def timed(fn):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(R):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(K):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / K * 1e3)
+    return statistics.median(ts), min(ts)
+
+
+x = torch.empty(2**28, device="cuda")
+y = torch.empty_like(x)
+for w in WORK:
+    if w in ("softmax", "rows_dense", "rows_literal"):
+        gen.fill_cuda(x, seed=1, dist="signed" if w == "softmax" else "unit")
+        xi, yo = x.view(65536, 4096), y.view(65536, 4096)
+        if w == "softmax":
+            fn = lambda: L.softmax_rows(yo, xi)  # noqa: E731
+        else:
+            idx = w.split("_")[1]
+            fn = lambda: L.normalize_rows(yo, xi, index=idx)  # noqa: E731
+    elif w in ("fused28", "dense28"):
+        gen.fill_cuda(x, seed=1, dist="unit")
+        idx = "literal" if w == "fused28" else "dense"
+        fn = lambda: L.normalize(y, x, index=idx)  # noqa: E731
+    elif w == "backprop":
+        n_in, hid = 2**22, 16
+        inp = torch.rand(n_in + 1, device="cuda")
+        hidden = torch.rand((n_in + 1) * (hid + 1), device="cuda")
+        outp = torch.empty(n_in, device="cuda")
+        fn = lambda: L.bpnn_layerforward(inp, hidden, outp, variant="tma")  # noqa: E731
+    else:
+        continue
+    med, mn = timed(fn)
+    print(f"{w:14s} median {med:9.2f} us  min {mn:9.2f} us", flush=True)
