@@ -114,7 +114,13 @@ __global__ void __launch_bounds__(256)
 constexpr int BPT_RUN = 15;                          // blocks per run: 240 items <= 256 consumers
 constexpr int BPT_HID_BYTES = 16384;                 // 15 * 1088 B + slack
 constexpr int BPT_STAGE = BPT_HID_BYTES + 1024;      // + 15 * 64 B of inputs + slack
-constexpr int BPT_STAGES = 4, BPT_CTAS = 2;
+#ifndef NORM_BPT_STAGES  // probe builds only (ring A/B): -DNORM_BPT_STAGES=6 -DNORM_BPT_CTAS=3
+#define NORM_BPT_STAGES 4
+#endif
+#ifndef NORM_BPT_CTAS
+#define NORM_BPT_CTAS 2
+#endif
+constexpr int BPT_STAGES = NORM_BPT_STAGES, BPT_CTAS = NORM_BPT_CTAS;
 constexpr size_t BPT_SMEM = (size_t)BPT_STAGES * BPT_STAGE;
 static_assert(BPT_RUN * 1088 + 16 <= BPT_HID_BYTES && BPT_RUN * 64 + 16 <= 1024, "a run fits a stage");
 static_assert(BPT_RUN * BP_H <= BK_CONSUMERS, "one item per consumer thread");

@@ -131,7 +131,10 @@ __global__ void __launch_bounds__(ROW_THREADS, row_ctas_per_sm(MAXV))
 // into `out`.  Up to S rows are in flight per SM, so HBM stays busy while each
 // warp finishes its row.
 constexpr int RB_MAX_STAGES = 16, RB_MAX_WARPS = 16;
-constexpr size_t RB_SMEM_BUDGET = 200 * 1024;
+#ifndef NORM_RB_BUDGET_KIB  // probe builds only (ring depth A/B): -DNORM_RB_BUDGET_KIB=128
+#define NORM_RB_BUDGET_KIB 200
+#endif
+constexpr size_t RB_SMEM_BUDGET = (size_t)NORM_RB_BUDGET_KIB * 1024;
 
 // ctr != NULL: the producer takes its grid-strided share of the first 97 % of the
 // rows, then claims rows of the rest from a queue (one ahead), tagging each stage
