@@ -15,7 +15,7 @@ cap() {  # name kernel_regex skip bench-args...
   ncu -i $OUT/$name.ncu-rep --page details --csv > $OUT/${name}_details.csv 2>/dev/null
 }
 cap reduce "reduce_dyn_kernel" 3 $B
-cap scale_dense "scale_bulk_kernel" 6 --index dense --numel 1073741824 $B
+cap scale_dense "scale_tile_kernel" 6 --index dense --numel 1073741824 $B
 cap fused28 "fused_kernel" 3 --workload paths28 --steps 3 --warmup 3
 cap rows_dense "rows_vec_kernel" 3 --workload rows --index dense --steps 3 --warmup 3
 cap rows_literal "rows_bulk_kernel" 3 --workload rows --index literal --steps 3 --warmup 3
@@ -25,7 +25,7 @@ cap mid "mid_kernel" 20 --workload small --steps 3 --warmup 3
 U="python scripts/ncu_traffic_update.py --json $OUT/ncu_traffic.json --capture ${TAG:-round2}"
 $U vector:literal $OUT/reduce_raw.csv reduce_dyn_kernel
 $U vector:dense $OUT/reduce_raw.csv reduce_dyn_kernel
-$U scale:dense $OUT/scale_dense_raw.csv scale_bulk_kernel
+$U scale:dense $OUT/scale_dense_raw.csv scale_tile_kernel
 $U paths28:literal $OUT/fused28_raw.csv fused_kernel
 $U rows:dense $OUT/rows_dense_raw.csv rows_vec_kernel
 $U rows:literal $OUT/rows_literal_raw.csv rows_bulk_kernel
