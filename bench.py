@@ -607,8 +607,8 @@ def run_vector(args, world, rank, local):
         # partials (same kernels, exchange over the process group); any failure or
         # mismatch falls back to NCCL and is recorded in the JSON line
         # Every rank runs the same sequence of collectives whatever fails locally
-        # (PeerComm agrees on set-up failures itself; the check below is one MIN
-        # all-reduce), so a failure on one rank cannot leave the others waiting
+        # (PeerComm agrees on set-up failures itself; the check below is one
+        # all-gather of the ranks' errors), so a failure on one rank cannot leave the others waiting
         # in a collective the failed rank never enters.
         import torch.distributed as dist
         err = None
@@ -630,12 +630,17 @@ def run_vector(args, world, rank, local):
                 err = err or f"gathered cross-check: {e}"
             if err is None and not torch.equal(s_p, s_g):
                 err = "p2p divisor != gathered divisor"
-            ok = torch.tensor([1.0 if err is None else 0.0], device=_dev() if _dev() == "cuda" else "cpu")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if ok.item() != 1.0:
-                err = err or "another rank's peer exchange failed"
+            if err is None and os.environ.get("NORM_BENCH_FAULT_P2P_RANK") == str(rank):
+                err = "injected fault (NORM_BENCH_FAULT_P2P_RANK, tests only)"
+            errs = [None] * world
+            dist.all_gather_object(errs, err)
+            bad = [f"rank {r}: {e}" for r, e in enumerate(errs) if e]
+            err = "; ".join(bad) if bad else None
         if err is not None:
-            exchange_note = f"p2p unavailable ({err}); fell back to nccl"
+            # NCCL on a real node; the caller-collective path when the ranks
+            # time-slice one GPU (NCCL refuses two ranks on one device)
+            fallback = "host" if _emulated() else "nccl"
+            exchange_note = f"p2p unavailable ({err}); fell back to {fallback}"
             print(f"[bench] {exchange_note}", file=sys.stderr)
             if comm is not None:
                 try:
@@ -643,7 +648,7 @@ def run_vector(args, world, rank, local):
                 except Exception:  # noqa: BLE001
                     pass
             comm = None
-            args.exchange = "nccl"
+            args.exchange = fallback
     if world > 1 and args.exchange in ("nccl", "nccl-allreduce") and comm is None:
         comm = L.Comm(allreduce=args.exchange == "nccl-allreduce")
     stream = torch.cuda.current_stream()

@@ -94,3 +94,26 @@ def test_bench_plain_python_launch_two_ranks():
     assert d["step_stats"]["rank_ms_max"] >= d["step_stats"]["rank_ms_min"] > 0
     # 2^24 + 7 elements split over 2 ranks: 32 MiB per rank < 4 x L2 -> flushed
     assert "flushed" in d["config"]["l2"]
+
+
+def test_bench_p2p_failure_on_one_rank_falls_back_everywhere():
+    """A peer-exchange failure seen by ONE rank (injected on rank 1 after the
+    cross-check) must move every rank to the same fallback exchange through the
+    same collectives (no rank left waiting in a collective the other skipped):
+    one JSON line, the fallback named in exchange_note, and a valid step."""
+    env_extra = {"NORM_BENCH_FAULT_P2P_RANK": "1"}
+    old = {k: os.environ.get(k) for k in env_extra}
+    os.environ.update(env_extra)
+    try:
+        d, _ = _torchrun(["--numel", str(2**24 + 7), "--steps", "3", "--warmup", "3", "--e2e-steps", "1"],
+                         timeout=300)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    note = d["config"]["exchange_note"]
+    assert note and "rank 1: injected fault" in note and "fell back to host" in note, note
+    assert d["config"]["exchange"] == "host"
+    assert d["n_gpus"] == 2 and d["value"] > 0
