@@ -20,6 +20,13 @@ for n, path in [(1000, "small"), (5000, "two_pass"), (2**20 + 7, "two_pass"), (2
         y = torch.zeros_like(x)
         s = torch.zeros(1, device="cuda")
         L.normalize(y, x, index=mode, path=path, sum_out=s)
+# scale_tile_kernel with a ragged head and tail, out of place and in place
+for off in (1, 5):
+    for n in (2**21 + 3, 70001):
+        base = torch.from_numpy(gen.make_host(n + 8, seed=2, dist=0)).cuda()
+        ob = torch.zeros_like(base)
+        L.normalize(ob[off:off + n], base[off:off + n], index="dense", path="two_pass")
+        L.normalize(base[off:off + n], base[off:off + n], index="literal", path="two_pass")
 for form in ("per_thread", "per_block"):
     x = torch.rand(3000, device="cuda"); y = torch.empty_like(x)
     L.normalize_form(y, x, form=form)
