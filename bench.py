@@ -1180,6 +1180,8 @@ def run_small(args, world, rank, local):
                           / R: the call with its input evicted from L2;
       python_us        -- back-to-back calls through the Python binding
                           (trusted pointers), wall time / call;
+      python_bound_us  -- the same through L.BoundNormalize (arguments
+                          marshalled once, one ctypes call per call);
       c_*              -- examples/latency_c: host enqueue and back-to-back wall
                           time per call from plain C, with and without libnorm's
                           pointer checks, and through a norm_graph_t replay;
@@ -1252,8 +1254,17 @@ def run_small(args, world, rank, local):
                 call()
             torch.cuda.synchronize()
             py = (time.perf_counter() - t0) / 2000 * 1e6
+            bound = L.BoundNormalize(out, x, index=args.index, path=path)
+            for _ in range(200):
+                bound()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(2000):
+                bound()
+            torch.cuda.synchronize()
+            py_bound = (time.perf_counter() - t0) / 2000 * 1e6
             res.append({"n": n, "path": path, "runs": chosen, "device_hot_us": hot, "device_flushed_us": fl,
-                        "python_us": py, "parity_ok": bool(ok)})
+                        "python_us": py, "python_bound_us": py_bound, "parity_ok": bool(ok)})
     # plain C: host enqueue / back-to-back per call
     cres = []
     exe = os.path.join(ROOT, "examples", "latency_c")

@@ -41,6 +41,7 @@ from ._lib import (  # noqa: F401
     normalize,
     normalize_form,
     NormGraph,
+    BoundNormalize,
     norm_graph_create,
     FORM,
     normalize_host,
@@ -60,7 +61,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "NormGraph", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes", "choose_path",
+    "normalize", "normalize_form", "NormGraph", "BoundNormalize", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes", "choose_path",
     "cache_release", "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

@@ -306,6 +306,44 @@ def bpnn_layerforward(input_units, hidden, output, variant="register", stream=No
     return hidden, output
 
 
+class BoundNormalize:
+    """One normalize call bound to fixed tensors for launch-bound Python callers
+    (configs 1-2: n = 1024, 2^20 + 7): the tensors are validated, the options
+    struct (stream, index, path, outputs, NORM_FLAG_TRUSTED_PTRS) built and the
+    ctypes argument tuple prepared once; each ``()`` is a single norm_launch_ex
+    call on the stream given at construction (default: the current stream then).
+    The tensors must stay alive and on their device; the device must be current
+    at call time (checked: a call on another device is refused, not launched).
+    Same kernels and results as ``normalize``."""
+
+    __slots__ = ("_keep", "_fn", "_args", "_dev")
+
+    def __init__(self, out, inp, index="literal", path="auto", stream=None, sum_out=None, sum_out_f64=None):
+        _check_f32(out, "out")
+        _check_f32(inp, "inp")
+        if not (out.is_contiguous() and inp.is_contiguous()) or out.numel() != inp.numel():
+            raise ValueError("out and inp must be contiguous with equal numel")
+        for t in (out, sum_out, sum_out_f64):
+            if t is not None and (not t.is_cuda or t.device != inp.device):
+                raise ValueError("every tensor must be on inp's CUDA device")
+        self._keep = (out, inp, sum_out, sum_out_f64)
+        o = _opts(index, path, stream, sum_out, sum_out_f64, None, inp.device, FLAG_TRUSTED_PTRS)
+        self._dev = inp.device.index if inp.device.index is not None else 0
+        self._fn = lib().norm_launch_ex
+        self._args = (ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(inp.data_ptr()),
+                      ctypes.c_int64(inp.numel()), ctypes.byref(o), o)
+
+    def __call__(self):
+        import torch
+        if torch.cuda.current_device() != self._dev:
+            raise ValueError(f"BoundNormalize: device {self._dev} is not current")
+        a = self._args
+        st = self._fn(a[0], a[1], a[2], a[3])
+        if st != 0:
+            raise NormError(st, last_error())
+        return self._keep[0]
+
+
 class NormGraph:
     """One normalize call captured as a CUDA graph (norm_graph_create): replay with
     launch(stream) -- one cudaGraphLaunch for the reduce + scale pair."""

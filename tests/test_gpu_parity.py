@@ -658,6 +658,24 @@ def test_graph_plan_matches_eager(n, mode, path):
     g.destroy()
 
 
+@pytest.mark.parametrize("n,mode,path", [(1024, "literal", "auto"), (2**20 + 7, "literal", "auto"),
+                                         (2**20 + 7, "dense", "two_pass"), (3000, "literal", "small")])
+def test_bound_normalize_matches_oracle(n, mode, path):
+    """L.BoundNormalize (arguments marshalled once) is the same norm_launch_ex call:
+    repeated calls give the oracle's replay bits, uncovered outputs untouched."""
+    xh = gen.make_host(n, seed=n % 97, dist=0)
+    x = to_dev(xh)
+    out = to_dev(sentinel(n))
+    s = torch.zeros(1, device="cuda")
+    b = L.BoundNormalize(out, x, index=mode, path=path, sum_out=s)
+    for _ in range(5):
+        b()
+    torch.cuda.synchronize()
+    check(xh, out.cpu().numpy(), np.float32(s.item()), mode, 0)
+    with pytest.raises(ValueError):
+        L.BoundNormalize(out, x.cpu())
+
+
 @pytest.mark.parametrize("n", [2**29 + 3, 2**31 - 5])
 def test_auto_fused_literal_mid_sizes(n):
     """AUTO takes the fused kernel for literal inputs larger than L2 whose covered
