@@ -107,7 +107,10 @@ __device__ __forceinline__ void sm_finish(float* dst, int nvr, f8* v, float* red
   }
 }
 
-__host__ __device__ constexpr int sm_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : 4; }
+#ifndef NORM_SM_CTAS  // probe builds only (occupancy A/B): -DNORM_SM_CTAS=5
+#define NORM_SM_CTAS 5
+#endif
+__host__ __device__ constexpr int sm_ctas_per_sm(int maxv) { return maxv >= 4 ? 2 : NORM_SM_CTAS; }
 
 // ctr != NULL: rows from a queue, as rows_vec_kernel (rows.cu): thread 0 claims
 // the row after next while the current row is finished and publishes it across

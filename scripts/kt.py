@@ -2,7 +2,7 @@
 the row and fused workloads, K back-to-back calls between CUDA events, median
 of R such groups, one line per workload (µs per call).  Much lighter than
 bench.py (no parity, e2e or CPU legs).  KT_WORK selects workloads
-(comma-separated: softmax, rows_dense, rows_literal, fused28, dense28, backprop)."""
+(comma-separated: softmax, logsoftmax, rows_dense, rows_literal, fused28, dense28, backprop)."""
 import os
 import statistics
 import sys
@@ -36,11 +36,12 @@ def timed(fn):
 x = torch.empty(2**28, device="cuda")
 y = torch.empty_like(x)
 for w in WORK:
-    if w in ("softmax", "rows_dense", "rows_literal"):
-        gen.fill_cuda(x, seed=1, dist="signed" if w == "softmax" else "unit")
+    if w in ("softmax", "logsoftmax", "rows_dense", "rows_literal"):
+        gen.fill_cuda(x, seed=1, dist="signed" if "softmax" in w else "unit")
         xi, yo = x.view(65536, 4096), y.view(65536, 4096)
-        if w == "softmax":
-            fn = lambda: L.softmax_rows(yo, xi)  # noqa: E731
+        if "softmax" in w:
+            lg = w == "logsoftmax"
+            fn = lambda: L.softmax_rows(yo, xi, log=lg)  # noqa: E731
         else:
             idx = w.split("_")[1]
             fn = lambda: L.normalize_rows(yo, xi, index=idx)  # noqa: E731
