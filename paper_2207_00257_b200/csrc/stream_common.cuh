@@ -14,10 +14,7 @@ namespace lnorm {
 constexpr int RED_THREADS = 512, RED_UNROLL = 4, RED_CTAS_PER_SM = 2;
 constexpr int SC_THREADS = 256, SC_UNROLL = 4, SC_CTAS_PER_SM = 4;
 constexpr int SMALL_THREADS = 1024;
-#ifndef NORM_ROW_CTAS  // probe builds only (occupancy A/B): -DNORM_ROW_CTAS=5
-#define NORM_ROW_CTAS 4
-#endif
-constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = NORM_ROW_CTAS;
+constexpr int ROW_THREADS = 256, ROW_MAXV = 4, ROW_CTAS_PER_SM = 4;
 constexpr int FU_SCALE_UNROLL = 8;  // fused phase 2 reads from L2: 256 B in flight per thread
 
 enum LoadKind { LD_STREAM = 0, LD_HINT = 1, LD_PLAIN = 2 };
