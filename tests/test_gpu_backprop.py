@@ -44,3 +44,21 @@ def test_bpnn_variants_agree_and_reject():
         assert torch.equal(h, res[0][0]) and torch.equal(o, res[0][1])
     with pytest.raises(L.NormError):
         L.bpnn_layerforward(x[:18], torch.zeros(18, 17, device="cuda"), torch.zeros(17, device="cuda"))
+
+
+def test_bpnn_bench_size_tma():
+    """The bench's launch configuration (in = 2^22, hid = 16, TMA form, run queue
+    over 148 x 2 CTAs): bitwise equal to the fp32 step-by-step oracle, twice in a
+    row (the queue counter resets itself between calls)."""
+    n_in = 2**22
+    x = gen.make_host(n_in + 1, seed=22, dist="signed")
+    w = gen.make_host((n_in + 1) * 17, seed=23, dist="unit").reshape(n_in + 1, 17)
+    hw_ref, out_ref = oracle.bpnn_layerforward(x, w)
+    xi = torch.from_numpy(x).cuda()
+    for _ in range(2):
+        hd = torch.from_numpy(w.copy()).cuda()
+        od = torch.full((n_in,), -3.0, device="cuda")
+        L.bpnn_layerforward(xi, hd, od, variant="tma")
+        torch.cuda.synchronize()
+        assert od.cpu().numpy().tobytes() == out_ref.tobytes()
+        assert hd.cpu().numpy().tobytes() == hw_ref.tobytes()
