@@ -89,11 +89,11 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   for (int64_t t = threadIdx.x; t < ntasks; t += BK_THREADS) v += __ldcg(task_sums + t);
   double S = block_sum(v, red);  // identical bits in every CTA
   if (post.mail) {
-    if (threadIdx.x == 0) {
-      if (blockIdx.x == 0) publish_partial(post, S);
+    if (threadIdx.x < 32) {  // warp 0: lane-parallel publish (CTA 0) and mailbox wait
+      if (blockIdx.x == 0) publish_partial_warp(post, S);
       double Sf;
-      combine_parts(mailbox, post.world, &Sf, post.epoch);
-      S_sh = Sf;
+      combine_parts_warp(mailbox, post.world, &Sf, post.epoch);
+      if (threadIdx.x == 0) S_sh = Sf;
     }
     __syncthreads();
     S = S_sh;
@@ -141,11 +141,11 @@ __global__ void __launch_bounds__(MID_THREADS, 1)
   for (int i = threadIdx.x; i < (int)gridDim.x; i += MID_THREADS) v += __ldcg(partials + i);
   double S = block_sum(v, red);  // identical bits in every CTA
   if (post.mail) {
-    if (threadIdx.x == 0) {
-      if (blockIdx.x == 0) publish_partial(post, S);
+    if (threadIdx.x < 32) {  // warp 0: lane-parallel publish (CTA 0) and mailbox wait
+      if (blockIdx.x == 0) publish_partial_warp(post, S);
       double Sf;
-      combine_parts(mailbox, post.world, &Sf, post.epoch);
-      S_sh = Sf;
+      combine_parts_warp(mailbox, post.world, &Sf, post.epoch);
+      if (threadIdx.x == 0) S_sh = Sf;
     }
     __syncthreads();
     S = S_sh;

@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(RED_THREADS, RED_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     *S_out = S;
     *ticket = 0u;  // leave the workspace reusable
-    publish_partial(post, S);
   }
+  if (threadIdx.x < 32) publish_partial_warp(post, S);
 }
 
 // Pass 1, TMA-bulk variant for n >= 2^22 (one CTA per SM), then the same
@@ -78,8 +78,8 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   if (threadIdx.x == 0) {
     *S_out = S;
     *ticket = 0u;
-    publish_partial(post, S);
   }
+  if (threadIdx.x < 32) publish_partial_warp(post, S);
 }
 
 #ifdef NORM_TIMELINE  // probe builds only (scripts/pdl_timeline.py): per-CTA %globaltimer stamps
@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     *S_out = S;
     *ticket = 0u;
     *task_ctr = 0u;
-    publish_partial(post, S);
   }
+  if (threadIdx.x < 32) publish_partial_warp(post, S);
   RED_STAMP(3);  // last CTA: S written
 }
 

@@ -28,13 +28,15 @@ __global__ void __launch_bounds__(SC_THREADS)
                  int nparts, float* sum_out, double* sum_out_f64, unsigned long long epoch) {
   __shared__ float s_sh;
   pdl_wait();  // S_parts are complete and visible; `in` is no longer being read
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S, epoch);
-    s_sh = s;
-    if (blockIdx.x == 0) {
-      if (sum_out) *sum_out = s;
-      if (sum_out_f64) *sum_out_f64 = S;
+    const float s = combine_parts_warp(S_parts, nparts, &S, epoch);
+    if (threadIdx.x == 0) {
+      s_sh = s;
+      if (blockIdx.x == 0) {
+        if (sum_out) *sum_out = s;
+        if (sum_out_f64) *sum_out_f64 = S;
+      }
     }
   }
   __syncthreads();
@@ -103,14 +105,16 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
   const int ct = threadIdx.x - 32;
   pdl_wait();
-  if (ct == 0) {
-    SCL_STAMP(2);  // griddepcontrol.wait returned: the reduce grid is complete
+  if (ct < 32) {  // consumer warp 0
+    if (ct == 0) SCL_STAMP(2);  // griddepcontrol.wait returned: the reduce grid is complete
     double S;
-    const float s = combine_parts(S_parts, nparts, &S, epoch);
-    s_sh = s;
-    if (blockIdx.x == 0) {
-      if (sum_out) *sum_out = s;
-      if (sum_out_f64) *sum_out_f64 = S;
+    const float s = combine_parts_warp(S_parts, nparts, &S, epoch);
+    if (ct == 0) {
+      s_sh = s;
+      if (blockIdx.x == 0) {
+        if (sum_out) *sum_out = s;
+        if (sum_out_f64) *sum_out_f64 = S;
+      }
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(BK_CONSUMERS) : "memory");  // consumers only
@@ -180,13 +184,15 @@ __global__ void __launch_bounds__(TILE_THREADS)
   f8 v;
   if (body) v = ALIAS ? ld8(in + off) : ld8_stream(in + off);
   pdl_wait();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S, epoch);
-    s_sh = s;
-    if (blockIdx.x == 0) {
-      if (sum_out) *sum_out = s;
-      if (sum_out_f64) *sum_out_f64 = S;
+    const float s = combine_parts_warp(S_parts, nparts, &S, epoch);
+    if (threadIdx.x == 0) {
+      s_sh = s;
+      if (blockIdx.x == 0) {
+        if (sum_out) *sum_out = s;
+        if (sum_out_f64) *sum_out_f64 = S;
+      }
     }
   }
   __syncthreads();
@@ -206,13 +212,15 @@ __global__ void __launch_bounds__(256)
                          double* sum_out_f64, unsigned long long epoch) {
   __shared__ float s_sh;
   pdl_wait();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double S;
-    const float s = combine_parts(S_parts, nparts, &S, epoch);
-    s_sh = s;
-    if (blockIdx.x == 0) {
-      if (sum_out) *sum_out = s;
-      if (sum_out_f64) *sum_out_f64 = S;
+    const float s = combine_parts_warp(S_parts, nparts, &S, epoch);
+    if (threadIdx.x == 0) {
+      s_sh = s;
+      if (blockIdx.x == 0) {
+        if (sum_out) *sum_out = s;
+        if (sum_out_f64) *sum_out_f64 = S;
+      }
     }
   }
   __syncthreads();

@@ -465,12 +465,19 @@ __device__ __forceinline__ double dyn_stream_sum(BulkRing<BK_STAGES, BK_CHUNK>& 
 // then one system-scope fence and the epoch flags (release).  Parity double
 // buffering makes a fast rank's next epoch unable to overwrite a slot that a slow
 // rank has not read yet (the next epoch's reduce needs this epoch's scale done).
-__device__ __forceinline__ void publish_partial(const PeerPost& post, double S) {
+// Warp-cooperative (call from all 32 lanes of ONE warp, S the same in every
+// lane): lane r stores the rank partial into rank r's mailbox, fences, then
+// release-stores rank r's flag, so the W remote stores and fences of a W-rank
+// exchange overlap instead of running one after another (one NVLink round trip
+// instead of W).  A reader that acquires rank r's flag needs only the value
+// store that precedes that flag's release in the same lane.
+__device__ __forceinline__ void publish_partial_warp(const PeerPost& post, double S) {
   if (!post.mail) return;
+  const int lane = threadIdx.x & 31;
   const size_t slot = ((size_t)(post.epoch & 1) * post.world + post.rank) * 2;
-  for (int r = 0; r < post.world; ++r) st_relaxed_sys_f64(post.mail[r] + slot, S);
+  for (int r = lane; r < post.world; r += 32) st_relaxed_sys_f64(post.mail[r] + slot, S);
   __threadfence_system();
-  for (int r = 0; r < post.world; ++r)
+  for (int r = lane; r < post.world; r += 32)
     st_release_sys_u64(reinterpret_cast<unsigned long long*>(post.mail[r] + slot + 1), post.epoch);
 }
 
@@ -478,31 +485,40 @@ __device__ __forceinline__ void publish_partial(const PeerPost& post, double S) 
 // epoch != 0, S_parts is this rank's mailbox: wait (acquire, system scope, ~30 s
 // timeout -> NaN) for every slot of parity epoch & 1 to carry `epoch`, then
 // combine the slots in rank order.  *S_full receives the fp64 sum.
-__device__ __forceinline__ float combine_parts(const double* S_parts, int nparts, double* S_full,
-                                              unsigned long long epoch = 0) {
-  double S;
-  if (epoch == 0) {
-    S = __ldcg(S_parts);
-    for (int r = 1; r < nparts; ++r) S += __ldcg(S_parts + r);  // fixed (rank / chunk) order
-  } else {
+// Warp-cooperative (call from all 32 lanes of ONE warp; every lane returns the
+// same value): lane r waits for / loads rank r's slot, so the W flag and value
+// round trips overlap; the sum is then taken in rank order through shuffles --
+// the same additions in the same order as a sequential loop, hence the same bits.
+__device__ __forceinline__ float combine_parts_warp(const double* S_parts, int nparts, double* S_full,
+                                                   unsigned long long epoch = 0) {
+  const int lane = threadIdx.x & 31;
+  const double* box = epoch == 0 ? S_parts : S_parts + (size_t)(epoch & 1) * nparts * 2;
+  const int stride = epoch == 0 ? 1 : 2;
+  bool ok = true;
+  if (epoch != 0) {
     // mailbox: wait for every rank's slot of this epoch (peer stores over NVLink)
-    const double* box = S_parts + (size_t)(epoch & 1) * nparts * 2;
     const unsigned long long t0 = globaltimer_ns();
-    bool ok = true;
-    for (int r = 0; r < nparts && ok; ++r) {
+    for (int r = lane; r < nparts && ok; r += 32) {
       const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(box + 2 * r + 1);
       while (ld_acquire_sys_u64(flag) != epoch) {
         if (globaltimer_ns() - t0 > 30000000000ull) { ok = false; break; }  // peer lost: no hang
         __nanosleep(64);
       }
     }
-    if (!ok) {
-      S = __longlong_as_double(0x7ff8000000000000ll);
-    } else {
-      S = ld_relaxed_sys_f64(box);
-      for (int r = 1; r < nparts; ++r) S += ld_relaxed_sys_f64(box + 2 * r);  // rank order
+    ok = __all_sync(0xffffffffu, ok);
+  }
+  double S = 0.0;
+  for (int base = 0; base < nparts; base += 32) {
+    const int r = base + lane;
+    double v = 0.0;
+    if (r < nparts) v = epoch == 0 ? __ldcg(box + r) : ld_relaxed_sys_f64(box + (size_t)stride * r);
+    const int m = nparts - base < 32 ? nparts - base : 32;
+    for (int j = 0; j < m; ++j) {  // fixed (rank / chunk) order
+      const double x = __shfl_sync(0xffffffffu, v, j);
+      S = (base == 0 && j == 0) ? x : S + x;
     }
   }
+  if (!ok) S = __longlong_as_double(0x7ff8000000000000ll);
   *S_full = S;
   return (float)S;  // RN to binary32
 }
