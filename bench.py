@@ -684,7 +684,12 @@ def run_vector(args, world, rank, local):
         kpath = "two_pass"
     fused_step = kpath in ("fused", "mid", "cluster")
     small_step = kpath == "small"
-    red_bytes = 4 * nloc + (8 * max(lloc, 0) if (fused_step or small_step) else 0)
+    # the kernel libnorm brackets with the bench events (norm_debug_set_events):
+    # the one kernel of a fused / mid / cluster / small step; on a two-pass step the
+    # reduce (4n), or at N = 1 the scale when it moves more (8|C| > 4n, dense)
+    scale_dom = (world == 1 and not (fused_step or small_step) and lloc >= 0 and 2 * lloc > nloc)
+    red_bytes = (8 * lloc if scale_dom else
+                 4 * nloc + (8 * max(lloc, 0) if (fused_step or small_step) else 0))
     # in-run calibration on the same buffers: a torch copy stream
     # (read + write bytes) and a torch read-only stream (torch.sum)
     calib = {}
@@ -788,6 +793,7 @@ def run_vector(args, world, rank, local):
              "mid_kernel (256-bit loads, grid barrier, exchange, scale: the whole step)" if kpath == "mid" else
              "fused_kernel (reduce + grid barrier + exchange + scale: the whole step)" if fused_step else
              "small_kernel (one CTA: sum, barrier, scale: the whole step)" if small_step else
+             "scale_tile_kernel (one 8 KiB tile per CTA: 8|C| of the step's 4n + 8|C| bytes)" if scale_dom else
              ("reduce_dyn_kernel (TMA-bulk reduce, dynamic deterministic tail)" if nloc >= (1 << 22)
               else "reduce_kernel") + " (the hoisted sum: 4n of the step's 4n + 8|C| bytes)")
     line = {
@@ -812,11 +818,13 @@ def run_vector(args, world, rank, local):
         "calibration": calib,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
-                     "traffic": load_traffic("vector", index) if (world == 1 and n == 2**32) else None,
+                     "traffic": (load_traffic("scale" if scale_dom else "vector", index)
+                                 if (world == 1 and n == 2**32) else None),
                      "kernel": kname,
                      "algorithmic_bytes_per_launch": red_bytes, "avg_launch_ms": red_ms_avg,
                      "share_of_step": red_ms_avg / ms_instr, "instrumented_ms_per_step": ms_instr,
-                     "frac_of_same_run_read_stream": (achieved / calib["torch_sum_gbs"]) if calib else None,
+                     ("frac_of_same_run_copy_stream" if scale_dom else "frac_of_same_run_read_stream"):
+                         (achieved / calib["torch_copy_gbs" if scale_dom else "torch_sum_gbs"]) if calib else None,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

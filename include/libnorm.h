@@ -365,8 +365,10 @@ norm_status_t norm_launch_sharded_peer(norm_peer_t* peer, float* out_local, cons
 /* Not part of the operation: for timing the dominant kernel (bench.py's
  * roofline).  begin / end are cudaEvent_t (or NULL).  Until called again, every
  * vector or sharded call made on THIS host thread records `begin` on its stream
- * immediately before its dominant kernel -- the reduce on two-pass paths, the
- * one kernel on the small and fused paths -- and `end` immediately after it.
+ * immediately before its dominant kernel -- on two-pass paths the reduce, or on
+ * one GPU the scale when it moves more algorithmic bytes (8|C| > 4n, e.g. the
+ * dense index); the one kernel on the small, mid, cluster and fused paths -- and
+ * `end` immediately after it.
  * (NULL, NULL) turns it off.  Ignored inside norm_graph_create. */
 norm_status_t norm_debug_set_events(void* begin, void* end);
 

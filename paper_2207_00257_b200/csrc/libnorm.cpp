@@ -375,19 +375,25 @@ static norm_status_t launch_vector(float* out, const float* in, const Coverage& 
     ev_end(st);
     return NORM_OK;
   }
+  // The step's dominant kernel for norm_debug_set_events: the reduce (4n bytes),
+  // or the scale when it moves more (8|C| > 4n: dense and nearly dense coverage).
+  const bool scale_dominant = cov.kind == COV_PREFIX && 2 * cov.L > cov.n;
   {
     NvtxRange r("libnorm:reduce");
-    ev_begin(st);
+    if (!scale_dominant) ev_begin(st);
     e = launch_reduce(in, cov.n, ws, ws.S, d, st);
     if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel launch");
-    ev_end(st);
+    if (!scale_dominant) ev_end(st);
   }
   NvtxRange r("libnorm:scale");
+  if (scale_dominant) ev_begin(st);
   if (cov.kind == COV_PREFIX)
     e = launch_scale(out, in, cov.L, ws.S, 1, o->sum_out, o->sum_out_f64, d, true, st, 0, ws.scale_ctr);
   else
     e = launch_scale_residue(out, in, cov.n, 0, cov.G, ws.S, 1, o->sum_out, o->sum_out_f64, true, st);
-  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "scale_kernel launch");
+  if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
+  if (scale_dominant) ev_end(st);
+  return NORM_OK;
 }
 
 // ----------------------------------------------------- host-buffer (e2e) path

@@ -15,7 +15,7 @@ cap() {  # name kernel_regex skip bench-args...
   ncu -i $OUT/$name.ncu-rep --page details --csv > $OUT/${name}_details.csv 2>/dev/null
 }
 cap reduce "reduce_dyn_kernel" 3 $B
-cap scale_dense "scale_tile_kernel" 6 --index dense --numel 1073741824 $B
+cap scale_dense "scale_tile_kernel" 6 --index dense $B
 cap fused28 "fused_kernel" 3 --workload paths28 --steps 3 --warmup 3
 cap rows_dense "rows_vec_kernel" 3 --workload rows --index dense --steps 3 --warmup 3
 cap rows_literal "rows_bulk_kernel" 3 --workload rows --index literal --steps 3 --warmup 3
