@@ -1,0 +1,42 @@
+"""bench.py at N = 1: the roofline object names the step's dominant kernel and
+its bytes: on a two-pass step the reduce (4n) for
+the literal index, the scale (8|C| = 8n) for the dense index, each measured with
+libnorm's own events around that kernel (norm_debug_set_events)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("index", ["literal", "dense"])
+def test_roofline_names_dominant_kernel(index):
+    n = 2**26
+    d = _bench(["--index", index, "--numel", str(n), "--path", "two_pass", "--steps", "5", "--warmup", "3",
+                "--no-e2e", "--no-cpu"])
+    r = d["roofline"]
+    assert d["config"]["path"] == "two_pass"
+    if index == "dense":
+        assert r["kernel"].startswith("scale_tile_kernel"), r["kernel"]
+        assert r["algorithmic_bytes_per_launch"] == 8 * n
+        assert r["share_of_step"] > 0.5
+    else:
+        assert r["kernel"].startswith("reduce"), r["kernel"]
+        assert r["algorithmic_bytes_per_launch"] == 4 * n
+        assert r["share_of_step"] > 0.7
+    assert 0 < r["avg_launch_ms"] < d["ms_per_step"] * 1.05
+    assert d["parity"]["ok"]
