@@ -989,9 +989,13 @@ def run_rows(args, world, rank, local):
                    "rows": R, "cols": C, "index": args.index, "algorithmic_bytes": algo,
                    "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
         "frac_of_hbm_peak": value / (world * peak),
-        "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
-                     "frac": value / world / peak, "traffic": load_traffic("rows", args.index),
-                     "kernel": "rows_kernel (single kernel per step)", "peak_source": src},
+        # one kernel per step; which one is libnorm's launch_rows rule for 4096-float
+        # rows: the TMA warp-per-row kernel when at most half of a row is covered
+        # (literal: 1120 of 4096), else the register kernel with the row queue
+        "roofline": single_kernel_roofline(
+            rl * (4 * C + 4 * cov), ms, peak, src,
+            ("rows_bulk_kernel (TMA warp-per-row)" if 2 * cov <= C else "rows_vec_kernel (register rows, row queue)")
+            + " -- the whole step", load_traffic("rows", args.index) if world == 1 else None),
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
