@@ -487,6 +487,37 @@ def exchange_record(L, name, out, inp, mine, n, index, world, args, flush):
             comm.destroy()
 
 
+def plan_record(L, comm, plan_name, n, index, world, rank, args, flush):
+    """The same sharded step under the OTHER literal shard plan (SURVEY §8(e):
+    report both): the coverage-balanced two-range plan, or the uniform one-range
+    plan in which rank 0 scales the whole covered prefix after the exchange.
+    Fresh buffers for this plan's ranges, same exchange, max over ranks."""
+    import torch
+    import gen
+    plan = L.plan_shards(n, world, index, plan_name == "balanced")
+    mine = plan[rank]
+    nloc = sum(ln for _, ln in mine)
+    inp = torch.empty(max(nloc, 1), dtype=torch.float32, device="cuda")[:nloc]
+    off = 0
+    for b, ln in mine:
+        gen.fill_cuda(inp[off:off + ln], seed=2207, dist="unit", offset=b)
+        off += ln
+    out = torch.empty_like(inp)
+    try:
+        step = sharded_step_fn(L, comm, out, inp, mine, n, index, world)
+        for _ in range(args.warmup):
+            step()
+        ms_local = time_steps(step, args.steps, world, flush)
+        ms = max_over_ranks(ms_local, world)
+        algo = L.algorithmic_bytes(n, index)
+        return {"plan": "coverage-balanced two-range" if plan_name == "balanced" else "uniform one-range",
+                "value": algo / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                "rank_ms_min": min_over_ranks(ms_local, world), "rank_ms_max": ms}
+    finally:
+        del inp, out
+        torch.cuda.empty_cache()
+
+
 def exchange_latency(L, names, world, index, reps=200):
     """Latency of one sharded normalize over a tiny vector (8192 elements per
     rank: the kernels are launch-bound, so the step is launch + exchange +
@@ -754,6 +785,12 @@ def run_vector(args, world, rank, local):
             extra["nccl_allreduce"] = alt["nccl-allreduce"]
         names = ["p2p", "host"] + ([] if _emulated() else ["nccl-allreduce", "nccl"])
         extra["exchange_latency"] = exchange_latency(L, names, world, index)
+        if index == "literal":  # both literal shard plans in one driver run
+            other = "uniform" if args.plan == "balanced" else "balanced"
+            try:
+                extra["other_shard_plan"] = plan_record(L, comm, other, n, index, world, rank, args, flush)
+            except Exception as e:  # noqa: BLE001
+                extra["other_shard_plan"] = {"plan": other, "unavailable": str(e)[:300]}
     # dense-index figure on the same buffers (caption reading R1), reported beside the headline
     if args.also_dense and index == "literal" and (world == 1 or comm is not None):
         dense_mine = L.plan_shards(n, world, "dense", True)[rank]

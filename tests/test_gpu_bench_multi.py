@@ -56,6 +56,9 @@ def test_bench_vector_two_ranks(exchange, n, plan):
     one = any(k in d["roofline"]["kernel"] for k in ("fused_kernel", "mid_kernel", "cluster_kernel"))
     assert d["gpu_launches"] == d["steps"] * (1 if one else 2)
     assert "cpu_baseline" not in d or d["cpu_baseline"] is None  # rank 0 at N = 1 only
+    other = d["other_shard_plan"]  # both literal shard plans measured in one run
+    assert other["plan"].startswith("uniform" if plan == "balanced" else "coverage-balanced"), other
+    assert other["value"] > 0 and other["rank_ms_max"] >= other["rank_ms_min"] > 0
 
 
 def test_bench_rows_two_ranks():
