@@ -293,6 +293,49 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same gradient in two launches (C % 8 == 0, 32 B-aligned rows): a zero
+// fill of the [N, C] tile with no loads at all -- one 2048-float tile of one row
+// per CTA on a non-persistent grid, so the block scheduler sweeps the gradient
+// as one contiguous write wavefront (the scale_tile_kernel pattern) -- then one
+// thread per row stores its one nonzero value over the zeros.  The scatter is
+// the fill's programmatic dependent: it loads target / weight / grad_out before
+// griddepcontrol.wait and stores after it.  Same fp64 arithmetic as
+// nll_backward_kernel, so the same bits.
+__global__ void __launch_bounds__(256)
+    nll_zero_tile_kernel(float* __restrict__ grad, int64_t C, int64_t ld, int64_t tiles_per_row) {
+  pdl_launch_dependents();  // the scatter may be scheduled as the last tiles drain
+  const int64_t r = blockIdx.x / tiles_per_row;
+  const int64_t c0 = (int64_t)(blockIdx.x % tiles_per_row) * 2048 + (int64_t)threadIdx.x * 8;
+  if (c0 >= C) return;
+  f8 z;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) z.v[j] = 0.0f;
+  st8_stream(grad + r * ld + c0, z);
+}
+
+__global__ void __launch_bounds__(256)
+    nll_scatter_kernel(float* __restrict__ grad, const float* __restrict__ grad_out,
+                       const int64_t* __restrict__ target, const float* __restrict__ weight,
+                       const float* __restrict__ total_weight, int64_t N, int64_t C, int64_t ld,
+                       int reduction, int64_t ignore_index) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool hit = false;
+  float val = 0.0f;
+  int64_t t = 0;
+  if (r < N) {  // inputs are not written by the zero fill: load them before the wait
+    t = target[r];
+    hit = t != ignore_index && t >= 0 && t < C;
+    if (hit) {
+      const double tw = reduction == NORM_REDUCTION_MEAN ? (double)*total_weight : 1.0;
+      const double go = reduction == NORM_REDUCTION_NONE ? (double)grad_out[r] : (double)grad_out[0];
+      const double w = weight ? (double)weight[t] : 1.0;
+      val = (float)(-w * go / tw);
+    }
+  }
+  pdl_wait();  // the zero fill of `grad` is complete
+  if (hit) grad[r * ld + t] = val;
+}
+
 // ============================================================ launchers
 
 cudaError_t launch_softmax_rows(float* out, const float* in, int64_t rows, int64_t cols,
@@ -346,6 +389,29 @@ cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_
                                 int64_t C, int64_t ld, int reduction, int64_t ignore_index,
                                 const DeviceInfo& d, cudaStream_t st) {
   const bool vec = (reinterpret_cast<uintptr_t>(grad) & 31u) == 0 && ld % 8 == 0 && C % 8 == 0;
+  // NORM_NLL_TILE=0: the persistent row loop below instead of the tile grid (A/B)
+  static const bool tile = [] {
+    const char* e = getenv("NORM_NLL_TILE");
+    return !(e && !strcmp(e, "0"));
+  }();
+  const int64_t tpr = (C + 2047) / 2048;
+  if (vec && tile && N > 0 && N <= 0x7fffffffll / tpr) {
+    const int threads = C < 2048 ? (int)((C / 8 + 31) / 32 * 32) : 256;
+    nll_zero_tile_kernel<<<(unsigned)(N * tpr), threads, 0, st>>>(grad, C, ld, tpr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};  // the scatter as the fill's programmatic dependent
+    cfg.gridDim = dim3((unsigned)((N + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_mode() != PDL_OFF ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, nll_scatter_kernel, grad, grad_out, target, weight, total_weight, N, C, ld,
+                              reduction, ignore_index);
+  }
   int64_t g = (int64_t)d.sms * 8;
   if (N < g) g = N;
   int threads = (int)((vec ? C / 8 : C) < 256 ? ((vec ? C / 8 : C) + 31) / 32 * 32 : 256);

@@ -2,7 +2,7 @@
 the row and fused workloads, K back-to-back calls between CUDA events, median
 of R such groups, one line per workload (µs per call).  Much lighter than
 bench.py (no parity, e2e or CPU legs).  KT_WORK selects workloads
-(comma-separated: softmax, logsoftmax, rows_dense, rows_literal, fused28, dense28, backprop)."""
+(comma-separated: softmax, logsoftmax, nllbwd, fill, rows_dense, rows_literal, fused28, dense28, backprop)."""
 import os
 import statistics
 import sys
@@ -49,6 +49,15 @@ for w in WORK:
         gen.fill_cuda(x, seed=1, dist="unit")
         idx = "literal" if w == "fused28" else "dense"
         fn = lambda: L.normalize(y, x, index=idx)  # noqa: E731
+    elif w == "nllbwd":  # ClassNLL backward: a 1 GiB write stream (zeros + one value per row)
+        nr, nc = 65536, 4096
+        tgt = (torch.rand(nr, device="cuda") * nc).long()
+        tw = torch.full((1,), float(nr), device="cuda")
+        g1 = torch.ones(1, device="cuda")
+        grad = y.view(nr, nc)
+        fn = lambda: L.nll_backward(g1, (nr, nc), tgt, tw, grad=grad)  # noqa: E731
+    elif w == "fill":  # context: torch's own write stream on the same 1 GiB
+        fn = lambda: y.fill_(1.5)  # noqa: E731
     elif w == "backprop":
         n_in, hid = 2**22, 16
         inp = torch.rand(n_in + 1, device="cuda")

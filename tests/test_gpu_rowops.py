@@ -4,6 +4,7 @@ fp64 oracle.  Tolerances: softmax per element 1e-5 relative
 total weight 1e-6 relative; NLL gradient 1e-6 relative on the target entries
 and exact zeros elsewhere; every kernel bitwise repeatable."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -120,3 +121,54 @@ def test_nll_edges():
     loss, _ = L.nll_forward(lp, t, None, "sum")
     torch.cuda.synchronize()
     assert math.isnan(loss.item())
+
+
+NLL_DRIVER = r"""
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import gen, paper_2207_00257_b200 as L
+out = sys.argv[1]
+for k, (N, C, pad, red) in enumerate([(4099, 1000, 16, "none"), (65536, 4096, 0, "mean"), (513, 2056, 8, "sum")]):
+    t = (gen.make_host(N, seed=k, dist="unit") * C).astype(np.int64)
+    t[::7] = -100
+    w = gen.make_host(C, seed=3, dist="unit") + np.float32(0.5)
+    buf = torch.full((N, C + pad), 7.0, device="cuda")
+    g = torch.from_numpy(gen.make_host(N, seed=11, dist="unit")).cuda() if red == "none" else torch.tensor([0.75], device="cuda")
+    tw = torch.tensor([float(N)], device="cuda")
+    L.nll_backward(g, (N, C), torch.from_numpy(t).cuda(), tw, torch.from_numpy(w).cuda(), red, grad=buf[:, :C])
+    torch.cuda.synchronize()
+    np.save(os.path.join(out, f"g{{k}}.npy"), buf.cpu().numpy())
+print("ok")
+"""
+
+
+def test_nll_backward_kernels_agree_padded(tmp_path):
+    """ClassNLL backward through the zero-fill + scatter pair (default) and the
+    persistent row kernel (NORM_NLL_TILE=0): bit-identical gradients, padding
+    columns untouched, and equal to the oracle's updateGradInput."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = NLL_DRIVER.format(root=root)
+    outs = []
+    for v in ("1", "0"):
+        d = tmp_path / f"t{v}"
+        d.mkdir()
+        r = subprocess.run([sys.executable, "-c", code, str(d)], env=dict(os.environ, NORM_NLL_TILE=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+        outs.append(d)
+    for k, (N, C, pad, red) in enumerate([(4099, 1000, 16, "none"), (65536, 4096, 0, "mean"), (513, 2056, 8, "sum")]):
+        a, b = np.load(outs[0] / f"g{k}.npy"), np.load(outs[1] / f"g{k}.npy")
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), k
+        assert np.all(a[:, C:] == 7.0), k
+        t = (gen.make_host(N, seed=k, dist="unit") * C).astype(np.int64)
+        t[::7] = -100
+        w = gen.make_host(C, seed=3, dist="unit") + np.float32(0.5)
+        g = gen.make_host(N, seed=11, dist="unit").astype(np.float64) if red == "none" else np.array([0.75])
+        gref = oracle.nll_backward(g, t, C, w, red, -100, float(N))
+        gv = a[:, :C].astype(np.float64)
+        nz = gref != 0
+        assert np.all(gv[~nz] == 0), k
+        assert np.all(np.abs(gv[nz] - gref[nz]) <= 1e-6 * np.abs(gref[nz])), k
