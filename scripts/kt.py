@@ -2,7 +2,7 @@
 the row and fused workloads, K back-to-back calls between CUDA events, median
 of R such groups, one line per workload (µs per call).  Much lighter than
 bench.py (no parity, e2e or CPU legs).  KT_WORK selects workloads
-(comma-separated: softmax, logsoftmax, nllbwd, fill, rows_dense, rows_literal, fused28, dense28, backprop)."""
+(comma-separated: softmax, logsoftmax, nllbwd, fill, dense30, dense30_inplace, rows_dense, rows_literal, fused28, dense28, backprop)."""
 import os
 import statistics
 import sys
@@ -45,6 +45,13 @@ for w in WORK:
         else:
             idx = w.split("_")[1]
             fn = lambda: L.normalize_rows(yo, xi, index=idx)  # noqa: E731
+    elif w in ("dense30", "dense30_inplace"):  # in-place vs out-of-place read+write streams
+        xs, ys = x[:2**28], y[:2**28]
+        gen.fill_cuda(xs, seed=1, dist="unit")
+        if w == "dense30":
+            fn = lambda: L.normalize(ys, xs, index="dense")  # noqa: E731
+        else:
+            fn = lambda: L.normalize(xs, xs, index="dense")  # noqa: E731
     elif w in ("fused28", "dense28"):
         gen.fill_cuda(x, seed=1, dist="unit")
         idx = "literal" if w == "fused28" else "dense"
