@@ -120,3 +120,15 @@ def test_bench_p2p_failure_on_one_rank_falls_back_everywhere():
     assert note and "rank 1: injected fault" in note and "fell back to host" in note, note
     assert d["config"]["exchange"] == "host"
     assert d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_sharded_example_two_ranks():
+    """examples/sharded_normalize.py (the README's multi-GPU usage) under
+    torch.distributed.run with 2 ranks on this GPU: the same divisor on both."""
+    env = dict(os.environ, NORM_EXAMPLE_BACKEND="gloo", NORM_EXAMPLE_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "examples", "sharded_normalize.py"), "--numel", str(2**24 + 7)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "identical on every rank: True" in r.stdout, r.stdout[-2000:]
