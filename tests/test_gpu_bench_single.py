@@ -40,3 +40,17 @@ def test_roofline_names_dominant_kernel(index):
         assert r["share_of_step"] > 0.5  # dominant (0.69-0.8 at 2^26, where launch costs weigh; 0.93 at 2^32)
     assert 0 < r["avg_launch_ms"] < d["ms_per_step"] * 1.05
     assert d["parity"]["ok"]
+
+
+def test_throttled_region_is_remeasured_once():
+    """Timing rule: a timed region that saw hw_slowdown (injected here) is
+    re-measured once; the line records the first attempt and reports the second."""
+    os.environ["NORM_BENCH_FAKE_THROTTLE"] = "1"
+    try:
+        d = _bench(["--numel", str(2**26), "--path", "two_pass", "--steps", "3", "--warmup", "3",
+                    "--no-e2e", "--no-cpu", "--no-parity"])
+    finally:
+        os.environ.pop("NORM_BENCH_FAKE_THROTTLE", None)
+    r = d["remeasured"]
+    assert "hw_slowdown" in r["first_reasons_rank0"] and r["first_ms_per_step"] > 0
+    assert d["ms_per_step"] > 0
