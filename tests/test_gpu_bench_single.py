@@ -54,3 +54,14 @@ def test_throttled_region_is_remeasured_once():
     r = d["remeasured"]
     assert "hw_slowdown" in r["first_reasons_rank0"] and r["first_ms_per_step"] > 0
     assert d["ms_per_step"] > 0
+
+
+@pytest.mark.parametrize("workload", ["rows", "softmax"])
+def test_large_row_workloads_follow_the_vector_timing_rule(workload):
+    """65536 x 4096 fp32 = 1 GiB of input >= 4 x L2: timed back to back like the
+    vector workload, with the flushed per-call ("isolated") time beside it."""
+    d = _bench(["--workload", workload, "--steps", "5", "--warmup", "3"])
+    assert "no flush" in d["config"]["l2"], d["config"]["l2"]
+    iso = d["isolated"]["ms_per_step"] if workload == "rows" else d["results"]["softmax"]["isolated_ms"]
+    # back to back hides the launch latency and ramp; it cannot be much slower than a cold call
+    assert 0 < d["ms_per_step"] < iso * 1.05, (d["ms_per_step"], iso)
