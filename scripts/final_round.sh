@@ -14,6 +14,7 @@ if [ -n "$NCU_KERNEL" ]; then
       python bench.py $NCU_WORKLOAD --steps 3 --warmup 3 > $OUT/k.bench.log 2>&1
   ncu -i $OUT/k.ncu-rep --page raw --csv > $OUT/k_raw.csv 2>/dev/null
   ncu -i $OUT/k.ncu-rep --page details --csv > $OUT/k_details.csv 2>/dev/null
+  ncu -i $OUT/k.ncu-rep --page source --csv > $OUT/k_source.csv 2>/dev/null
   rm -f $OUT/k.ncu-rep
   python scripts/ncu_traffic_update.py --json $OUT/ncu_traffic.json --capture ${TAG:-final} $NCU_KEY \
       $OUT/k_raw.csv $NCU_KERNEL
