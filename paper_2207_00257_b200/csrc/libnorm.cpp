@@ -735,6 +735,10 @@ NORM_API norm_status_t norm_softmax_rows(float* out, const float* in, int64_t ro
                                          const norm_opts_t* o) {
   if (!o) o = &kDefaultOpts;
   if (kind != NORM_SOFTMAX && kind != NORM_LOG_SOFTMAX) return fail(NORM_ERR_INVALID_VALUE, "bad kind");
+  {
+    const norm_status_t so = check_opts(o);
+    if (so != NORM_OK) return so;
+  }
   if (rows < 0 || cols < 0) return fail(NORM_ERR_INVALID_VALUE, "rows < 0 or cols < 0");
   if (ld_out < cols || ld_in < cols) return fail(NORM_ERR_INVALID_VALUE, "ld < cols");
   if (rows == 0 || cols == 0) return NORM_OK;
@@ -770,10 +774,18 @@ NORM_API norm_status_t norm_nll_forward(float* loss, float* total_weight, const 
   if (!o) o = &kDefaultOpts;
   norm_status_t s;
   if ((s = check_nll(N, C, ld, reduction)) != NORM_OK) return s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
   if (!loss || (N > 0 && (!logp || !target))) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
   if (reduction == NORM_REDUCTION_NONE && N == 0) return NORM_OK;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
+  // every pointer the kernels dereference: device memory of this device
+  if ((s = check_device_ptr(loss, "loss", d, o)) != NORM_OK) return s;
+  if (total_weight && (s = check_device_ptr(total_weight, "total_weight", d, o)) != NORM_OK) return s;
+  if (weight && (s = check_device_ptr(weight, "weight", d, o)) != NORM_OK) return s;
+  if (N > 0 && ((s = check_device_ptr(logp, "logp", d, o)) != NORM_OK ||
+                (s = check_device_ptr(target, "target", d, o)) != NORM_OK))
+    return s;
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Workspace ws;
   if ((s = get_workspace(o, d.device, st, &ws)) != NORM_OK) return s;
@@ -793,8 +805,15 @@ NORM_API norm_status_t norm_nll_backward(float* grad, const float* grad_out, con
   if (!grad || !grad_out || !target) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
   if (reduction == NORM_REDUCTION_MEAN && !total_weight)
     return fail(NORM_ERR_INVALID_VALUE, "MEAN needs total_weight");
+  if ((s = check_opts(o)) != NORM_OK) return s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(grad, "grad", d, o)) != NORM_OK ||
+      (s = check_device_ptr(grad_out, "grad_out", d, o)) != NORM_OK ||
+      (s = check_device_ptr(target, "target", d, o)) != NORM_OK)
+    return s;
+  if (weight && (s = check_device_ptr(weight, "weight", d, o)) != NORM_OK) return s;
+  if (total_weight && (s = check_device_ptr(total_weight, "total_weight", d, o)) != NORM_OK) return s;
   cudaError_t e = launch_nll_backward(grad, grad_out, target, weight, total_weight, N, C, ld,
                                       reduction, ignore_index, d, static_cast<cudaStream_t>(o->stream));
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "nll_backward launch");
@@ -813,8 +832,13 @@ NORM_API norm_status_t norm_bpnn_layerforward(const float* input, float* hidden,
   if (!input || !hidden || !output) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer");
   if (in / 16 > 2147483647LL) return fail(NORM_ERR_UNSUPPORTED, "too many blocks");
   norm_status_t s;
+  if ((s = check_opts(o)) != NORM_OK) return s;
   DeviceInfo d;
   if ((s = check_device(&d)) != NORM_OK) return s;
+  if ((s = check_device_ptr(input, "input", d, o)) != NORM_OK ||
+      (s = check_device_ptr(hidden, "hidden", d, o)) != NORM_OK ||
+      (s = check_device_ptr(output, "output", d, o)) != NORM_OK)
+    return s;
   Workspace ws;
   if ((s = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return s;
   cudaError_t e = launch_bpnn(input, hidden, output, in, hid, variant,

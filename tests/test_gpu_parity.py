@@ -353,6 +353,35 @@ def test_host_pointer_rejected():
     torch.cuda.synchronize()
 
 
+def test_host_pointer_rejected_by_row_ops_and_backprop():
+    """The softmax, ClassNLL and backprop entries validate every pointer their
+    kernels dereference like the normalize entries do: a host buffer is
+    NORM_ERR_INVALID_VALUE, not a sticky device fault (the context stays usable)."""
+    import ctypes
+    lib = L.lib()
+    bad = L._lib.STATUS.index("NORM_ERR_INVALID_VALUE")
+    h = torch.ones(64 * 17)
+    ht = torch.zeros(64, dtype=torch.int64)
+    d = torch.ones(64 * 17, device="cuda")
+    dt = torch.zeros(64, dtype=torch.int64, device="cuda")
+    dl = torch.zeros(64, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    assert lib.norm_softmax_rows(P(d), P(h), 4, 16, 16, 16, 0, None) == bad
+    # nll forward: host logp / host target / host loss
+    assert lib.norm_nll_forward(P(dl), None, P(h), P(dt), None, 64, 16, 16, 1, -100, None) == bad
+    assert lib.norm_nll_forward(P(dl), None, P(d), P(ht), None, 64, 16, 16, 1, -100, None) == bad
+    assert lib.norm_nll_forward(P(h), None, P(d), P(dt), None, 64, 16, 16, 1, -100, None) == bad
+    # nll backward: host grad / host target
+    assert lib.norm_nll_backward(P(h), P(dl), P(dt), None, None, 64, 16, 16, 2, -100, None) == bad
+    assert lib.norm_nll_backward(P(d), P(dl), P(ht), None, None, 64, 16, 16, 2, -100, None) == bad
+    # backprop layer-forward: host hidden weights
+    assert lib.norm_bpnn_layerforward(P(d), P(h), P(dl), 48, 16, 3, None) == bad
+    torch.cuda.synchronize()  # no fault was raised
+    y = torch.empty(16, device="cuda")
+    L.normalize(y, torch.ones(16, device="cuda"), index="dense")
+    assert torch.allclose(y, torch.full_like(y, 1 / 16))
+
+
 @pytest.mark.slow
 def test_full_size_2_32_sampled():
     """BASELINE configs[3] at W = 1, the launch bench.py times: literal two-pass."""
