@@ -419,6 +419,62 @@ def test_full_size_2_32_sampled():
     assert np.array_equal(tail, x[n - 4099:] / sv2)
 
 
+@pytest.mark.slow
+def test_max_size_2_35_in_place_sampled():
+    """The largest input one B200 holds in place: n = 2^35 + 13 fp32 (128 GiB, not a
+    multiple of 32; offsets past 2^34 bytes).  Literal then dense, in place (the
+    aliasing reading: S over the original input, uncovered elements untouched).
+    The oracle's exact sum is taken over the same seeded input regenerated on the
+    host in 256 MiB chunks on every host core (chunk sums correctly rounded,
+    combined with fsum); the
+    outputs are checked bitwise by replay on windows at the head, around the
+    covered prefix's end, at random offsets and at the tail."""
+    n = 2**35 + 13
+    free, _ = torch.cuda.mem_get_info()
+    if free < 4 * n + (2 << 30):
+        pytest.skip(f"needs {4 * n / 2**30:.0f} GiB free on the device")
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    import os
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    chunk = 1 << 26
+    local = threading.local()
+
+    def part(b):  # the ctypes calls release the GIL: one chunk per host core at a time
+        if not hasattr(local, "buf"):
+            local.buf = np.empty(chunk, dtype=np.float32)
+        m = min(chunk, n - b)
+        gen.fill_host(local.buf[:m], seed=2207, dist=0, offset=b)
+        return oracle.sum_exact(local.buf[:m])
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        parts = list(ex.map(part, range(0, n, chunk)))
+    S = math.fsum(parts)
+    count, L_ = oracle.coverage_closed(n)
+    assert L_ == (n + 31) // 32 + 992
+    rng = np.random.default_rng(35)
+    wins = [0, L_ - 4096, L_, n - 4099] + [int(v) for v in rng.integers(0, n - 4096, 48)]
+
+    def window(b):
+        return gen.make_host(min(4096, n - b), seed=2207, dist=0, offset=b)
+
+    for mode in ("literal", "dense"):
+        gen.fill_cuda(x, seed=2207, dist=0)
+        s = torch.zeros(1, device="cuda")
+        L.normalize(x, x, index=mode, sum_out=s)
+        torch.cuda.synchronize()
+        sv = np.float32(s.item())
+        assert abs(float(sv) - S) <= 1e-6 * S, (mode, float(sv), S)
+        cov_end = L_ if mode == "literal" else n
+        for b in wins:
+            xin = window(b)
+            got = x[b:b + xin.size].cpu().numpy()
+            idx = np.arange(b, b + xin.size)
+            want = np.where(idx < cov_end, xin / sv, xin).astype(np.float32)
+            assert got.view(np.uint32).tobytes() == want.view(np.uint32).tobytes(), (mode, b)
+    del x
+    torch.cuda.empty_cache()
+
+
 def test_empty_and_degenerate():
     e = torch.empty(0, device="cuda")
     L.normalize(e, e)
