@@ -861,13 +861,17 @@ def run_vector(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, world, rank, local, mine, n, index)
-    parity = None
-    if not args.no_parity and world == 1:
-        parity = parity_record(L, out, inp, n, index, SENTINEL_BITS)
     launches_per_step = 1 if (fused_step or small_step) else 2
+    # The cpu_baseline leg (rank 0 at N = 1, after every GPU measurement) -- with
+    # --impl reference the only place bench.py runs oracle/: the oracle timed on a
+    # bounded sample, and the benched launch's parity against the oracle.
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(index)
+        if not args.no_parity:
+            parity = parity_record(L, out, inp, n, index, SENTINEL_BITS)
+            parity["leg"] = "cpu_baseline (oracle on the host, after the GPU measurements)"
     meta = run_meta(world)
     if rank != 0:
         return
@@ -1266,11 +1270,11 @@ def run_small(args, world, rank, local):
                           time per call from plain C, with and without libnorm's
                           pointer checks, and through a norm_graph_t replay;
       parity           -- each path's output vs the oracle (exact S within 1e-6,
-                          bitwise replay, uncovered outputs untouched)."""
+                          bitwise replay, uncovered outputs untouched), taken in
+                          the cpu_baseline leg after every GPU measurement."""
     import numpy as np
     import torch
     import gen
-    import oracle
     import paper_2207_00257_b200 as L
     stream = torch.cuda.current_stream()
     ws = torch.zeros(L.workspace_bytes(), dtype=torch.uint8, device="cuda")
@@ -1302,7 +1306,7 @@ def run_small(args, world, rank, local):
         return a.elapsed_time(b) * 1e3 / reps
 
     res = []
-    ok_all = True
+    outputs = []
     for n in (1024, 2**20 + 7):
         xh = gen.make_host(n, seed=2207, dist="unit")
         x = torch.from_numpy(xh).cuda()
@@ -1314,16 +1318,13 @@ def run_small(args, world, rank, local):
 
             def call():
                 L.normalize(out, x, index=args.index, path=path, workspace=ws, trusted=True)
-            # parity of this path (sentinel-filled output, then one call)
+            # this path's output for the parity check of the cpu_baseline leg
+            # (sentinel-filled output, then one call)
             out.view(torch.int32).fill_(SENTINEL_BITS)
             s = torch.zeros(1, device="cuda")
             L.normalize(out, x, index=args.index, path=path, workspace=ws, sum_out=s)
             torch.cuda.synchronize()
-            o, sv, S = out.cpu().numpy(), np.float32(s.item()), oracle.sum_exact(xh)
-            sent = np.full(n, SENTINEL_BITS, np.uint32).view(np.float32)
-            rep = oracle.replay(xh, sv, args.index, out=sent.copy())
-            ok = abs(float(sv) - S) <= 1e-6 * S and np.array_equal(o.view(np.uint32), rep.view(np.uint32))
-            ok_all &= bool(ok)
+            outputs.append((xh, out.cpu().numpy(), np.float32(s.item())))
             hot = graph_us(lambda: [call() for _ in range(R)]) / R
             fl = (graph_us(lambda: [(flush(), call()) for _ in range(20)]) / 20) - t_flush
             for _ in range(200):
@@ -1344,7 +1345,7 @@ def run_small(args, world, rank, local):
             torch.cuda.synchronize()
             py_bound = (time.perf_counter() - t0) / 2000 * 1e6
             res.append({"n": n, "path": path, "runs": chosen, "device_hot_us": hot, "device_flushed_us": fl,
-                        "python_us": py, "python_bound_us": py_bound, "parity_ok": bool(ok)})
+                        "python_us": py, "python_bound_us": py_bound})
     # plain C: host enqueue / back-to-back per call
     cres = []
     exe = os.path.join(ROOT, "examples", "latency_c")
@@ -1355,6 +1356,30 @@ def run_small(args, world, rank, local):
         for c in cres:
             if c.get("n") == row["n"] and c.get("path") == row["path"]:
                 row.update({("c_" + k): v for k, v in c.items() if k not in ("n", "path", "runs")})
+    # cpu_baseline leg (after every GPU measurement; the only use of oracle/ here):
+    # each path's output against the oracle, and the oracle's own time per call
+    parity = cpu = None
+    if not args.no_cpu:
+        import oracle
+        ok_all = True
+        for row, (xh, o, sv) in zip(res, outputs):
+            S = oracle.sum_exact(xh)
+            sent = np.full(xh.size, SENTINEL_BITS, np.uint32).view(np.float32)
+            rep = oracle.replay(xh, sv, args.index, out=sent.copy())
+            ok = abs(float(sv) - S) <= 1e-6 * S and np.array_equal(o.view(np.uint32), rep.view(np.uint32))
+            row["parity_ok"] = bool(ok)
+            ok_all &= bool(ok)
+        parity = {"ok": ok_all, "leg": "cpu_baseline (oracle on the host, after the GPU measurements)",
+                  "what": "per path and size: |s - S| <= 1e-6 S and the whole output == oracle_replay(x, s) bitwise"}
+        xh = gen.make_host(1024, seed=2207, dist="unit")
+        ob = np.empty_like(xh)
+        oracle.form_hoisted(xh, args.index, out=ob)
+        t0 = time.perf_counter()
+        for _ in range(2000):
+            oracle.form_hoisted(xh, args.index, out=ob)
+        cpu = {"value": (time.perf_counter() - t0) / 2000 * 1e6, "unit": "us per call", "cores": 1,
+               "kind": "oracle", "sample": "oracle form 3 (hoisted) at n = 1024, 2000 calls from Python (ctypes), "
+                                           "1 thread"}
     head = next(r for r in res if r["n"] == 1024 and r["path"] == "auto")
     value = head.get("c_trusted_back_to_back_us", head["python_us"])
     line = {"metric": "normalize latency per call, configs 1-2 (n=1024 32x32 literal grid; n=2^20+7)",
@@ -1364,8 +1389,7 @@ def run_small(args, world, rank, local):
             "config": {"workload": f"normalize n=1024 and n=2^20+7 fp32 (Fig. 1), {args.index} index, every path",
                        "l2": "device_hot_us: input L2-resident; device_flushed_us: 256 MiB write + 256 MiB read "
                              "before every call inside the graph, flush time subtracted"},
-            "results": res, "parity": {"ok": ok_all, "what": "per path and size: |s - S| <= 1e-6 S and the whole "
-                                                              "output == oracle_replay(x, s) bitwise"},
+            "results": res, "parity": parity, "cpu_baseline": cpu,
             "gpu_launches": len(res) * R}
     if rank == 0:
         emit(line)

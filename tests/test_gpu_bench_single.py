@@ -27,7 +27,7 @@ def _bench(args):
 def test_roofline_names_dominant_kernel(index):
     n = 2**28  # large enough that launch gaps do not blur the shares (at 2^26 the dense scale measured 0.497-0.6)
     d = _bench(["--index", index, "--numel", str(n), "--path", "two_pass", "--steps", "5", "--warmup", "3",
-                "--no-e2e", "--no-cpu"])
+                "--no-e2e"])  # the parity record is taken in the cpu_baseline leg
     r = d["roofline"]
     assert d["config"]["path"] == "two_pass"
     if index == "dense":

@@ -44,3 +44,31 @@ def test_libnorm_does_not_link_the_oracle():
     assert not any("oracle" in n or "normgen" in n for n in needed), needed
     syms = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
     assert "oracle_" not in syms
+
+
+def test_bench_runs_the_oracle_only_in_its_cpu_legs():
+    """bench.py may execute oracle/ only in the cpu_baseline leg (which also takes
+    the parity record, after every GPU measurement) and the --impl reference arm:
+    every function that imports it is one of those, and the GPU arms call the
+    parity check only from inside a `not args.no_cpu` block."""
+    import ast
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    tree = ast.parse(src)
+    importers = set()
+    for fn in ast.walk(tree):
+        if isinstance(fn, ast.FunctionDef):
+            for node in ast.walk(fn):
+                if isinstance(node, ast.Import) and any(a.name == "oracle" for a in node.names):
+                    importers.add(fn.name)
+    # oracle_bytes / oracle_sample / parity_record: the cpu_baseline leg's helpers;
+    # run_reference: the reference arm; run_small / run_licm: their lines' cpu legs
+    assert importers <= {"oracle_bytes", "oracle_sample", "parity_record", "run_reference", "run_small",
+                         "run_licm"}, importers
+    # the module itself never imports it at top level
+    assert not any(isinstance(n, ast.Import) and any(a.name == "oracle" for a in n.names) for n in tree.body)
+    # parity_record is called only under `if ... not args.no_cpu:`
+    calls = [m.start() for m in re.finditer(r"(?<!def )parity_record\(L,", src)]
+    assert calls
+    for c in calls:
+        block = src[:c].rsplit("\n    if ", 1)[-1]
+        assert "not args.no_cpu" in block.split("\n")[0], block.split("\n")[0]
