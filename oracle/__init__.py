@@ -55,6 +55,8 @@ def lib():
         L.oracle_nll_backward.argtypes = [vp, vp, vp, vp, ctypes.c_double, i64, i64, i64,
                                           ctypes.c_int, i64]
         L.oracle_bpnn_layerforward.argtypes = [vp, vp, vp, i64, i64]
+        L.oracle_normalize_backward.argtypes = [vp, vp, vp, ctypes.c_double, i64, ctypes.c_int]
+        L.oracle_softmax_backward_rows.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -238,6 +240,40 @@ def nll_backward(grad_out, target, C, weight=None, reduction="mean", ignore_inde
                                    N, C, C, RED[reduction], ignore_index)
     assert rc == 0
     return grad
+
+
+# ------------------------------------------------ gradients (autograd of the ops)
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def normalize_backward(g, y, S, mode="literal"):
+    """d(sum g*y)/dx of the functional normalize y = normalize(x) (uncovered y_j = x_j),
+    from g, y and the divisor S, in fp64: gx_j = [j in C] g_j / S + [j not in C] g_j -
+    sum_{i in C} g_i y_i / S."""
+    g, y = _f64(g), _f64(y)
+    gx = np.empty_like(g)
+    assert lib().oracle_normalize_backward(gx.ctypes.data, g.ctypes.data, y.ctypes.data, float(S),
+                                           g.size, _mode(mode)) == 0
+    return gx
+
+
+def rows_normalize_backward(g2d, y2d, S_rows, mode="literal"):
+    """normalize_backward of every row (row r with its own divisor S_rows[r])."""
+    g2d, y2d = _f64(g2d), _f64(y2d)
+    return np.stack([normalize_backward(g2d[r], y2d[r], S_rows[r], mode) for r in range(g2d.shape[0])]) \
+        if g2d.shape[0] else np.empty_like(g2d)
+
+
+def softmax_backward_rows(g2d, y2d, log=False):
+    """Row softmax gradient y (g - sum g y), or log-softmax g - exp(y) sum g, in fp64."""
+    g2d, y2d = _f64(g2d), _f64(y2d)
+    R, C = g2d.shape
+    gx = np.empty_like(g2d)
+    assert lib().oracle_softmax_backward_rows(gx.ctypes.data, g2d.ctypes.data, y2d.ctypes.data, R, C,
+                                              int(bool(log))) == 0
+    return gx
 
 
 # ------------------------------------------------ NEXT-4: backprop layerforward

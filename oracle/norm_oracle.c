@@ -463,6 +463,41 @@ int oracle_nll_backward(double* grad, const double* grad_out, const int64_t* tar
   return 0;
 }
 
+/* ------------------------------------------------------------ gradients
+ * For PyTorch autograd of the forward ops above (the training the paper runs
+ * through MocCUDA).  Plain derivatives, fp64 in and out.
+ *
+ * normalize (functional form y = normalize(x): covered y_i = x_i / S with
+ * S = sum_{k<n} x_k; uncovered y_j = x_j): with g = dL/dy and
+ * y_i = x_i / S,  dy_i/dx_j = [i == j]/S - x_i/S^2 for i in C(n), so
+ *   gx_j = [j in C] g_j / S + [j not in C] g_j - D,   D = sum_{i in C} g_i y_i / S. */
+int oracle_normalize_backward(double* gx, const double* g, const double* y, double S, int64_t n,
+                              int mode) {
+  if (n < 0 || (n > 0 && (!gx || !g || !y))) return 1;
+  double D = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    if (oracle_is_covered(n, mode, i)) D += g[i] * y[i];
+  D /= S;
+  for (int64_t j = 0; j < n; ++j) gx[j] = (oracle_is_covered(n, mode, j) ? g[j] / S : g[j]) - D;
+  return 0;
+}
+
+/* softmax: y = exp(x - m) / sum exp(x - m)  ->  gx_j = y_j (g_j - sum_k g_k y_k);
+ * log-softmax: y = x - m - log sum exp(x - m)  ->  gx_j = g_j - exp(y_j) sum_k g_k. */
+int oracle_softmax_backward_rows(double* gx, const double* g, const double* y, int64_t rows,
+                                 int64_t cols, int log_softmax) {
+  if (rows < 0 || cols < 0 || (rows > 0 && cols > 0 && (!gx || !g || !y))) return 1;
+  for (int64_t r = 0; r < rows; ++r) {
+    const double* gr = g + r * cols;
+    const double* yr = y + r * cols;
+    double D = 0.0;
+    for (int64_t k = 0; k < cols; ++k) D += log_softmax ? gr[k] : gr[k] * yr[k];
+    for (int64_t j = 0; j < cols; ++j)
+      gx[r * cols + j] = log_softmax ? gr[j] - exp(yr[j]) * D : yr[j] * (gr[j] - D);
+  }
+  return 0;
+}
+
 /* ================================================================ NEXT-4
  * bpnn_layerforward of Rodinia backprop as printed in Fig. backprop
  * (PAPER.md:553-579).  The printed listing elides the index expressions and

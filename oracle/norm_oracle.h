@@ -92,6 +92,13 @@ enum { ORACLE_RED_NONE = 0, ORACLE_RED_MEAN = 1, ORACLE_RED_SUM = 2 };
  * ignored); SUM: loss[0] = sum l_i; MEAN: loss[0] = sum l_i / sum w[t_i] (NaN if
  * the weight sum is 0).  *total_weight = sum w[t_i].  A target outside [0, C) that
  * is not ignore_index gives NaN (reading R17). */
+/* Gradients (fp64): y = normalize(x) in its functional form (uncovered y_j = x_j),
+ * given g = dL/dy, y and S: gx_j = [j in C] g_j / S + [j not in C] g_j - sum_{i in C} g_i y_i / S. */
+int oracle_normalize_backward(double* gx, const double* g, const double* y, double S, int64_t n,
+                              int mode);
+/* softmax: gx = y (g - sum g y); log-softmax: gx = g - exp(y) sum g (rows x cols, contiguous). */
+int oracle_softmax_backward_rows(double* gx, const double* g, const double* y, int64_t rows,
+                                 int64_t cols, int log_softmax);
 int oracle_nll_forward(double* loss, double* total_weight, const float* logp, const int64_t* target,
                        const float* weight, int64_t N, int64_t C, int64_t ld, int reduction,
                        int64_t ignore_index);
