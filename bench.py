@@ -1160,6 +1160,35 @@ def run_softmax(args, world, rank, local):
         tms, tiso, _ = timed_calls(lambda: fn(inp, dim=1), args.steps, 4 * R * C, flush, stream)
         res[("log_softmax" if log else "softmax") + "_torch"] = {"ms_per_step": tms, "isolated_ms": tiso,
                                                                  "value": 8 * R * C / (tms / 1e3) / 1e9}
+    # gradients (norm_softmax_rows_backward, norm_rows_backward): read g and y, write gx
+    g = torch.empty_like(inp)
+    gen.fill_cuda(g.view(-1), seed=2208, dist="signed")
+    gx = torch.empty_like(inp)
+    for log in (False, True):
+        L.softmax_rows(out, inp, log=log)
+        for _ in range(args.warmup):
+            L.softmax_rows_backward(gx, g, out, log=log)
+        ms, iso, _ = timed_calls(lambda: L.softmax_rows_backward(gx, g, out, log=log), args.steps, 8 * R * C,
+                                 flush, stream)
+        nm = "log_softmax_backward" if log else "softmax_backward"
+        res[nm] = {"ms_per_step": ms, "isolated_ms": iso, "value": 12 * R * C / (ms / 1e3) / 1e9,
+                   "frac": 12 * R * C / (ms / 1e3) / 1e9 / peak}
+        for _ in range(args.warmup):
+            torch._softmax_backward_data(g, out, 1, torch.float32) if not log else \
+                torch._log_softmax_backward_data(g, out, 1, torch.float32)
+        tms, tiso, _ = timed_calls(
+            (lambda: torch._log_softmax_backward_data(g, out, 1, torch.float32)) if log else
+            (lambda: torch._softmax_backward_data(g, out, 1, torch.float32)), args.steps, 8 * R * C, flush, stream)
+        res[nm + "_torch"] = {"ms_per_step": tms, "isolated_ms": tiso, "value": 12 * R * C / (tms / 1e3) / 1e9}
+    srow = torch.zeros(R, device="cuda")
+    L.normalize_rows(out, inp.abs(), index="dense", sum_out=srow)
+    for _ in range(args.warmup):
+        L.normalize_rows_backward(gx, g, out, srow, index="dense")
+    ms, iso, _ = timed_calls(lambda: L.normalize_rows_backward(gx, g, out, srow, index="dense"), args.steps,
+                             8 * R * C, flush, stream)
+    res["rows_normalize_backward_dense"] = {"ms_per_step": ms, "isolated_ms": iso,
+                                            "value": 12 * R * C / (ms / 1e3) / 1e9,
+                                            "frac": 12 * R * C / (ms / 1e3) / 1e9 / peak}
     # ClassNLLCriterion on the same shape (log-probs = log_softmax output)
     L.softmax_rows(out, inp, log=True)
     tgt = torch.empty(R, dtype=torch.float32, device="cuda")

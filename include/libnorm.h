@@ -216,6 +216,31 @@ norm_status_t norm_nll_backward(float* grad, const float* grad_out, const int64_
                                 int64_t C, int64_t ld, int32_t reduction, int64_t ignore_index,
                                 const norm_opts_t* o);
 
+/* ------------------------------------------- gradients (autograd of the ops above)
+ * The paper runs PyTorch training through its transpiled kernels (MocCUDA,
+ * PAPER.md:710-753); these are the backward passes of the forward entries, used
+ * by the torch.library ops' autograd.  Each is one fp64 reduction (fixed order,
+ * bit-identical run to run) and one elementwise fp32 pass.  g = dL/dy, y = the
+ * forward's output; gx may be g or y itself (exact alias), partial overlap of gx
+ * with g or y -> NORM_ERR_OVERLAP.  All pointers are device memory of the current
+ * device; stream-ordered on o->stream like the forward calls.
+ *
+ * Functional normalize, y = x with y[C(n)] = x[C(n)] / s (the forward on a copy
+ * of x, or in place; o->index selects C(n)), s = the forward's divisor (device
+ * fp32[1], e.g. its sum_out), PAPER.md:108-110:
+ *   gx_j = ([j in C] ? g_j / s : g_j) - D,   D = sum_{i in C} g_i y_i / s. */
+norm_status_t norm_launch_backward(float* gx, const float* g, const float* y, const float* s,
+                                   int64_t n, const norm_opts_t* o);
+/* The same per row of a [rows][ld] matrix (C(cols) per row), s = fp32[rows] divisors
+ * (norm_rows's sum_out). */
+norm_status_t norm_rows_backward(float* gx, const float* g, const float* y, const float* s,
+                                 int64_t rows, int64_t cols, int64_t ld, const norm_opts_t* o);
+/* Row softmax: gx = y (g - sum_k g_k y_k); log-softmax (kind NORM_LOG_SOFTMAX):
+ * gx = g - exp(y) sum_k g_k.  [rows][ld] matrices (PyTorch's _softmax_backward_data). */
+norm_status_t norm_softmax_rows_backward(float* gx, const float* g, const float* y, int64_t rows,
+                                         int64_t cols, int64_t ld, int32_t kind,
+                                         const norm_opts_t* o);
+
 /* ------------------------------- backprop layerforward (NEXT-4) */
 typedef enum {
   NORM_BP_PRINTED = 0,     /* Fig. backprop as printed: shared memory, 8 barriers             */

@@ -20,6 +20,9 @@ from ._lib import (  # noqa: F401
     norm_nll_forward,
     norm_nll_backward,
     norm_bpnn_layerforward,
+    norm_launch_backward,
+    norm_rows_backward,
+    norm_softmax_rows_backward,
     norm_coverage,
     norm_algorithmic_bytes,
     norm_choose_path,
@@ -47,6 +50,9 @@ from ._lib import (  # noqa: F401
     normalize_host,
     normalize_rows,
     softmax_rows,
+    normalize_backward,
+    normalize_rows_backward,
+    softmax_rows_backward,
     bpnn_layerforward,
     BP_VARIANT,
     nll_forward,
@@ -61,7 +67,7 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "normalize", "normalize_form", "NormGraph", "BoundNormalize", "FORM", "normalize_rows", "softmax_rows", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes", "choose_path",
+    "normalize", "normalize_form", "NormGraph", "BoundNormalize", "FORM", "normalize_rows", "softmax_rows", "normalize_backward", "normalize_rows_backward", "softmax_rows_backward", "bpnn_layerforward", "BP_VARIANT", "nll_forward", "nll_backward", "REDUCTION", "normalize_host", "coverage", "algorithmic_bytes", "choose_path",
     "cache_release", "plan_shards", "normalize_sharded_via", "workspace_bytes", "Comm", "PeerComm", "NormError", "lib", "status_string",
     "last_error", "INDEX", "PATH",
 ]

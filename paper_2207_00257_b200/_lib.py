@@ -63,6 +63,9 @@ def lib():
             "norm_nll_forward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
             "norm_nll_backward": [vp, vp, vp, vp, vp, i64, i64, i64, i32, i64, optp],
             "norm_rows": [vp, vp, i64, i64, i64, i64, optp],
+            "norm_launch_backward": [vp, vp, vp, vp, i64, optp],
+            "norm_rows_backward": [vp, vp, vp, vp, i64, i64, i64, optp],
+            "norm_softmax_rows_backward": [vp, vp, vp, i64, i64, i64, i32, optp],
             "norm_coverage": [i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "norm_workspace_bytes": [i64, optp, ctypes.POINTER(ctypes.c_size_t)],
             "norm_algorithmic_bytes": [i64, i32, ctypes.POINTER(i64)],
@@ -394,6 +397,54 @@ def normalize_rows(out, inp, index="literal", stream=None, sum_out=None, sum_out
     return out
 
 
+def _check_same(ts, names, shape=None):
+    ref = ts[0]
+    for t, nm in zip(ts, names):
+        _check_f32(t, nm)
+        if t.device != ref.device or t.shape != ref.shape or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous tensor of {tuple(ref.shape)} on {ref.device}")
+
+
+def normalize_backward(gx, g, y, s, index="literal", stream=None):
+    """Gradient of the functional normalize y = normalize(x) (norm_launch_backward):
+    gx = ([j in C] ? g / s : g) - sum_{i in C} g_i y_i / s.  s: the forward's 1-element
+    divisor tensor.  gx may be g or y.  Returns gx."""
+    _check_same([gx, g, y], ["gx", "g", "y"])
+    _check_f32(s, "s")
+    o = _opts(index, "auto", stream, None, None, device=g.device)
+    with _call(g.device):
+        _check(lib().norm_launch_backward(gx.data_ptr(), g.data_ptr(), y.data_ptr(), s.data_ptr(), g.numel(),
+                                          ctypes.byref(o)))
+    return gx
+
+
+def normalize_rows_backward(gx, g, y, s, index="literal", stream=None):
+    """Row-wise normalize_backward of contiguous 2-D tensors (norm_rows_backward); s: the
+    forward's per-row divisors (float32[rows])."""
+    _check_same([gx, g, y], ["gx", "g", "y"])
+    _check_f32(s, "s")
+    if g.dim() != 2 or s.numel() != g.shape[0]:
+        raise ValueError("2-D g / y / gx and one divisor per row")
+    o = _opts(index, "auto", stream, None, None, device=g.device)
+    with _call(g.device):
+        _check(lib().norm_rows_backward(gx.data_ptr(), g.data_ptr(), y.data_ptr(), s.data_ptr(), g.shape[0],
+                                        g.shape[1], g.shape[1], ctypes.byref(o)))
+    return gx
+
+
+def softmax_rows_backward(gx, g, y, log=False, stream=None):
+    """Row softmax gradient y (g - sum g y), or log-softmax g - exp(y) sum g, of contiguous
+    2-D tensors (norm_softmax_rows_backward).  gx may be g or y.  Returns gx."""
+    _check_same([gx, g, y], ["gx", "g", "y"])
+    if g.dim() != 2:
+        raise ValueError("2-D tensors expected")
+    o = _opts("literal", "auto", stream, None, None, device=g.device)
+    with _call(g.device):
+        _check(lib().norm_softmax_rows_backward(gx.data_ptr(), g.data_ptr(), y.data_ptr(), g.shape[0],
+                                                g.shape[1], g.shape[1], 1 if log else 0, ctypes.byref(o)))
+    return gx
+
+
 def normalize_host(out, inp, index="literal", stream=None, sum_out=None, sum_out_f64=None):
     """End-to-end entry on HOST buffers (norm_launch_host): CPU float32 tensors or numpy
     arrays (pin them for overlapped copies).  Enqueued on `stream`; synchronise it
@@ -612,6 +663,12 @@ def norm_softmax_rows(out, inp, kind="softmax", stream=None):
     return softmax_rows(out, inp, log=(kind in ("log_softmax", 1)), stream=stream)
 
 
+def norm_softmax_rows_backward(gx, g, y, kind="softmax", stream=None):
+    return softmax_rows_backward(gx, g, y, log=(kind in ("log_softmax", 1)), stream=stream)
+
+
+norm_launch_backward = normalize_backward
+norm_rows_backward = normalize_rows_backward
 norm_graph_create = NormGraph
 norm_nll_forward = nll_forward
 norm_nll_backward = nll_backward

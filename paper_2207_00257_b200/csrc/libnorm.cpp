@@ -760,6 +760,82 @@ NORM_API norm_status_t norm_softmax_rows(float* out, const float* in, int64_t ro
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "softmax kernel launch");
 }
 
+// ---- gradients (backward.cu) ----
+// gx may alias g or y exactly; any other overlap of gx with g or y is rejected.
+static norm_status_t check_bwd_spans(const float* gx, const float* g, const float* y, size_t span) {
+  if (gx != g && partial_overlap(gx, span, g, span)) return fail(NORM_ERR_OVERLAP, "gx and g overlap");
+  if (gx != y && partial_overlap(gx, span, y, span)) return fail(NORM_ERR_OVERLAP, "gx and y overlap");
+  return NORM_OK;
+}
+
+static norm_status_t check_bwd_ptrs(const float* gx, const float* g, const float* y, const float* s,
+                                    const DeviceInfo& d, const norm_opts_t* o) {
+  norm_status_t st;
+  if ((st = check_device_ptr(gx, "gx", d, o)) != NORM_OK || (st = check_device_ptr(g, "g", d, o)) != NORM_OK ||
+      (st = check_device_ptr(y, "y", d, o)) != NORM_OK)
+    return st;
+  if (s && (st = check_device_ptr(s, "s", d, o)) != NORM_OK) return st;
+  return NORM_OK;
+}
+
+NORM_API norm_status_t norm_launch_backward(float* gx, const float* g, const float* y, const float* s,
+                                            int64_t n, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  norm_status_t st;
+  if ((st = check_opts(o)) != NORM_OK) return st;
+  if (n < 0) return fail(NORM_ERR_INVALID_VALUE, "n < 0");
+  if (n == 0) return NORM_OK;
+  if (!gx || !g || !y || !s) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer with n > 0");
+  if (!aligned4(gx) || !aligned4(g) || !aligned4(y) || !aligned4(s))
+    return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  if ((st = check_bwd_spans(gx, g, y, (size_t)n * 4)) != NORM_OK) return st;
+  const Coverage cov = coverage_of(n, o->index);
+  DeviceInfo d;
+  if ((st = check_device(&d)) != NORM_OK) return st;
+  if ((st = check_bwd_ptrs(gx, g, y, s, d, o)) != NORM_OK) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(o->stream);
+  Workspace ws;
+  if ((st = get_workspace(o, d.device, stream, &ws)) != NORM_OK) return st;
+  NvtxRange r("norm_launch_backward");
+  const cudaError_t e = launch_normalize_backward(gx, g, y, s, cov, ws, d, stream);
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "normalize backward launch");
+}
+
+static norm_status_t rows_backward(float* gx, const float* g, const float* y, const float* s,
+                                   int64_t rows, int64_t cols, int64_t ld, int kind, const norm_opts_t* o) {
+  norm_status_t st;
+  if ((st = check_opts(o)) != NORM_OK) return st;
+  if (rows < 0 || cols < 0) return fail(NORM_ERR_INVALID_VALUE, "rows < 0 or cols < 0");
+  if (ld < cols) return fail(NORM_ERR_INVALID_VALUE, "ld < cols");
+  if (rows == 0 || cols == 0) return NORM_OK;
+  if (!gx || !g || !y || (kind == BW_NORMALIZE && !s)) return fail(NORM_ERR_INVALID_VALUE, "NULL pointer with work to do");
+  if (!aligned4(gx) || !aligned4(g) || !aligned4(y) || (s && !aligned4(s)))
+    return fail(NORM_ERR_INVALID_VALUE, "pointer not 4-byte aligned");
+  if ((st = check_bwd_spans(gx, g, y, (size_t)((rows - 1) * ld + cols) * 4)) != NORM_OK) return st;
+  DeviceInfo d;
+  if ((st = check_device(&d)) != NORM_OK) return st;
+  if ((st = check_bwd_ptrs(gx, g, y, kind == BW_NORMALIZE ? s : nullptr, d, o)) != NORM_OK) return st;
+  const Coverage rc = coverage_of(cols, o->index);
+  NvtxRange r("norm_rows_backward");
+  const cudaError_t e = launch_rows_backward(gx, g, y, s, rows, cols, ld, kind, rc, d,
+                                             static_cast<cudaStream_t>(o->stream));
+  return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows backward launch");
+}
+
+NORM_API norm_status_t norm_rows_backward(float* gx, const float* g, const float* y, const float* s,
+                                          int64_t rows, int64_t cols, int64_t ld, const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  return rows_backward(gx, g, y, s, rows, cols, ld, BW_NORMALIZE, o);
+}
+
+NORM_API norm_status_t norm_softmax_rows_backward(float* gx, const float* g, const float* y, int64_t rows,
+                                                  int64_t cols, int64_t ld, int32_t kind,
+                                                  const norm_opts_t* o) {
+  if (!o) o = &kDefaultOpts;
+  if (kind != NORM_SOFTMAX && kind != NORM_LOG_SOFTMAX) return fail(NORM_ERR_INVALID_VALUE, "bad kind");
+  return rows_backward(gx, g, y, nullptr, rows, cols, ld, kind == NORM_SOFTMAX ? BW_SOFTMAX : BW_LOG_SOFTMAX, o);
+}
+
 static norm_status_t check_nll(int64_t N, int64_t C, int64_t ld, int32_t reduction) {
   if (N < 0 || C < 1 || ld < C) return fail(NORM_ERR_INVALID_VALUE, "need N >= 0, C >= 1, ld >= C");
   if (reduction < NORM_REDUCTION_NONE || reduction > NORM_REDUCTION_SUM)

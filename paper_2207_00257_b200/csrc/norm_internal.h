@@ -161,6 +161,14 @@ cudaError_t launch_nll_backward(float* grad, const float* grad_out, const int64_
                                 const float* weight, const float* total_weight, int64_t N,
                                 int64_t C, int64_t ld, int reduction, int64_t ignore_index,
                                 const DeviceInfo& d, cudaStream_t st);
+// Gradients (backward.cu): normalize's functional form and row softmax / log-softmax.
+enum BwKind { BW_NORMALIZE = 0, BW_SOFTMAX = 1, BW_LOG_SOFTMAX = 2 };
+cudaError_t launch_normalize_backward(float* gx, const float* g, const float* y, const float* s,
+                                      const Coverage& cov, const Workspace& ws, const DeviceInfo& d,
+                                      cudaStream_t st);
+cudaError_t launch_rows_backward(float* gx, const float* g, const float* y, const float* s_rows,
+                                 int64_t rows, int64_t cols, int64_t ld, int kind, const Coverage& rc,
+                                 const DeviceInfo& d, cudaStream_t st);
 
 // NEXT-4 backprop layerforward (backprop.cu)
 cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_t in, int64_t hid,
