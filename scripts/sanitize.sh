@@ -47,6 +47,25 @@ for v in ("printed", "eliminated", "register", "tma"):
 for C in (512, 1024, 8192, 12288):
     x = torch.rand(37, C, device="cuda"); y = torch.zeros_like(x)
     L.normalize_rows(y, x, index="literal")
+# gradient kernels (backward.cu): vector (aligned / misaligned, both index modes, in
+# place), rows (vector and scalar paths), softmax / log-softmax
+for n, off in ((5000, 0), (2**20 + 7, 0), (70001, 1), (100, 0)):
+    for mode in ("literal", "dense"):
+        xb = torch.rand(n + 8, device="cuda") + 0.1; gb = torch.randn(n + 8, device="cuda")
+        yv = xb[off:off + n].clone(); sv = torch.zeros(1, device="cuda")
+        L.normalize(yv, yv, index=mode, sum_out=sv)
+        gxv = torch.empty(n + 8, device="cuda")[off:off + n]
+        L.normalize_backward(gxv, gb[off:off + n], yv, sv, index=mode)
+        gi = gb[off:off + n].clone(); L.normalize_backward(gi, gi, yv, sv, index=mode)
+for (R, C) in [(300, 4096), (7, 1001), (3, 4099)]:
+    xr = torch.rand(R, C, device="cuda") + 0.1; gr = torch.randn(R, C, device="cuda")
+    for mode in ("literal", "dense"):
+        yr = xr.clone(); sr = torch.zeros(R, device="cuda")
+        L.normalize_rows(yr, yr, index=mode, sum_out=sr)
+        L.normalize_rows_backward(torch.empty_like(gr), gr, yr, sr, index=mode)
+    for lg in (False, True):
+        ys = torch.empty_like(xr); L.softmax_rows(ys, xr, log=lg)
+        L.softmax_rows_backward(torch.empty_like(gr), gr, ys, log=lg)
 h = torch.rand(2**20 + 7).pin_memory(); o = torch.zeros_like(h).pin_memory()
 L.normalize_host(o, h)
 torch.cuda.synchronize()
