@@ -1115,13 +1115,32 @@ def run_paths28(args, world, rank, local):
         algo = L.algorithmic_bytes(n, args.index)
         res[path] = {"ms_per_step": ms, "value": algo / (ms / 1e3) / 1e9, "frac": algo / (ms / 1e3) / 1e9 / peak}
     best = max(res, key=lambda k: res[k]["value"])
+    # the gradient at the same n (norm_launch_backward): a dot over the covered set
+    # (reads g, y there) and an elementwise pass (reads g, writes gx): 8|C| + 8n bytes
+    y = inp.clone()
+    s = torch.zeros(1, device="cuda")
+    L.normalize(y, y, index=args.index, sum_out=s)
+    g = torch.empty_like(inp)
+    gen.fill_cuda(g, seed=2208, dist="signed")
+    gx = torch.empty_like(inp)
+    for _ in range(args.warmup):
+        L.normalize_backward(gx, g, y, s, index=args.index)
+    bms, biso, bnote = timed_calls(lambda: L.normalize_backward(gx, g, y, s, index=args.index), args.steps,
+                                   8 * n, flush, stream)
+    cov, _ = L.coverage(n, args.index)
+    bbytes = 8 * cov + 8 * n
+    backward = {"ms_per_step": bms, "isolated_ms": biso, "value": bbytes / (bms / 1e3) / 1e9,
+                "frac": bbytes / (bms / 1e3) / 1e9 / peak, "bytes": bbytes, "l2": bnote,
+                "kernels": "vec_bwd_dot_kernel + vec_bwd_apply_kernel"}
+    del y, g, gx
     line = {"metric": "normalize GB/s and % of HBM peak (n=2^28, two-pass vs fused)",
             "value": res[best]["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res[best]["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"normalize n=2^28 fp32, {args.index}, best path = {best}",
                        "l2": "flushed before every step (256 MiB write, then a 256 MiB read so the write-back happens outside the timed region)"},
-            "paths": res, "peak": peak, "gpu_launches": args.steps * 3}  # two-pass (2 kernels) + fused (1) per step
+            "paths": res, "backward": backward, "peak": peak,
+            "gpu_launches": args.steps * 3}  # two-pass (2 kernels) + fused (1) per step
     if best == "fused":
         line["roofline"] = single_kernel_roofline(
             L.algorithmic_bytes(n, args.index), res["fused"]["ms_per_step"], peak, src,

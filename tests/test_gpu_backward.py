@@ -224,3 +224,23 @@ def test_backward_writes_stay_in_bounds():
             torch.cuda.synchronize()
             assert guards_ok(buf, R * C, 0), (R, C, kind)
             assert not torch.any(gx.reshape(-1).view(torch.int32) == SENT)
+
+
+def test_autograd_under_torch_compile():
+    """The differentiable ops trace under torch.compile(fullgraph=True) (fake kernels
+    for the forward and the backward ops) and give the eager gradients bit for bit."""
+    import paper_2207_00257_b200.torch_ops  # noqa: F401  (registers the ops)
+
+    def f(x, w):
+        y, s = torch.ops.libnorm.normalize_fwd(x, "literal")
+        return (y * w).sum() + torch.ops.libnorm.softmax(x.view(8, -1), True).sum()
+
+    cf = torch.compile(f, fullgraph=True)
+    base = torch.from_numpy(gen.make_host(8 * 512, seed=12, dist="unit")).cuda()
+    w = torch.from_numpy(gen.make_host(8 * 512, seed=13, dist="signed")).cuda()
+    x1 = base.clone().requires_grad_()
+    cf(x1, w).backward()
+    x2 = base.clone().requires_grad_()
+    f(x2, w).backward()
+    torch.cuda.synchronize()
+    assert torch.equal(x1.grad, x2.grad)
