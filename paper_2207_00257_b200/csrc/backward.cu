@@ -23,7 +23,13 @@
 namespace lnorm {
 
 constexpr int BW_THREADS = 256;
-constexpr int BW_ROW_CTAS_PER_SM = 8;
+#ifndef NORM_BW_MINB  // probe builds only (occupancy A/B)
+#define NORM_BW_MINB 4
+#endif
+#ifndef NORM_BW_ROW_CTAS
+#define NORM_BW_ROW_CTAS 8
+#endif
+constexpr int BW_ROW_CTAS_PER_SM = NORM_BW_ROW_CTAS;
 
 __device__ __forceinline__ bool bw_cov(int64_t i, int64_t L, int64_t G) {
   return L >= 0 ? i < L : (i % 32) < G;
@@ -83,7 +89,7 @@ __device__ __forceinline__ float4 bw_out4(const float4& a, const float4& b, int6
 // sweep 1 reduces the row, sweep 2 (same element-to-thread map, so gx may alias
 // g or y) writes it.  VEC: float4 accesses (16-byte aligned rows, cols % 4 == 0).
 template <int KIND, bool VEC>
-__global__ void __launch_bounds__(BW_THREADS, 4)
+__global__ void __launch_bounds__(BW_THREADS, NORM_BW_MINB)
     rows_bwd_kernel(float* gx, const float* g, const float* y, const float* s_rows, int64_t rows,
                     int64_t cols, int64_t ld, int64_t L, int64_t G) {
   __shared__ double red[2][BW_THREADS / 32];
@@ -197,11 +203,20 @@ __global__ void __launch_bounds__(BW_THREADS, 4)
     const int64_t n4 = n >> 2;
     const float4* g4 = reinterpret_cast<const float4*>(g);
     float4* x4 = reinterpret_cast<float4*>(gx);
-#pragma unroll 4
-    for (int64_t j = tid; j < n4; j += nth) {
+    // four float4 loads in flight per thread before their stores (gx may alias g:
+    // each element is loaded before it is stored, by the same thread)
+    int64_t j = tid;
+    for (; j + 3 * nth < n4; j += 4 * nth) {
+      float4 a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] = __ldcs(g4 + j + k * nth);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        __stcs(x4 + j + k * nth, bw_out4<BW_NORMALIZE>(a[k], a[k], 4 * (j + k * nth), L, G, D, dv));
+    }
+    for (; j < n4; j += nth) {
       const float4 a = __ldcs(g4 + j);
-      const int64_t e = 4 * j;
-      __stcs(x4 + j, bw_out4<BW_NORMALIZE>(a, a, e, L, G, D, dv));
+      __stcs(x4 + j, bw_out4<BW_NORMALIZE>(a, a, 4 * j, L, G, D, dv));
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
       const int64_t e = 4 * n4 + threadIdx.x;

@@ -2,7 +2,8 @@
 the row and fused workloads, K back-to-back calls between CUDA events, median
 of R such groups, one line per workload (µs per call).  Much lighter than
 bench.py (no parity, e2e or CPU legs).  KT_WORK selects workloads
-(comma-separated: softmax, logsoftmax, nllbwd, fill, dense30, dense30_inplace, rows_dense, rows_literal, fused28, dense28, backprop)."""
+(comma-separated: softmax, logsoftmax, nllbwd, fill, dense30, dense30_inplace, rows_dense, rows_literal, fused28, dense28, backprop,
+smbwd, lsmbwd, rowsbwd, vecbwd28l, vecbwd28d)."""
 import os
 import statistics
 import sys
@@ -71,6 +72,27 @@ for w in WORK:
         hidden = torch.rand((n_in + 1) * (hid + 1), device="cuda")
         outp = torch.empty(n_in, device="cuda")
         fn = lambda: L.bpnn_layerforward(inp, hidden, outp, variant="tma")  # noqa: E731
+    elif w in ("smbwd", "lsmbwd", "rowsbwd", "vecbwd28l", "vecbwd28d"):  # gradient kernels
+        gen.fill_cuda(x, seed=1, dist="signed")
+        gg = torch.empty_like(x)
+        gen.fill_cuda(gg, seed=2, dist="signed")
+        gxo = torch.empty_like(x)
+        if w in ("smbwd", "lsmbwd"):
+            lg = w == "lsmbwd"
+            L.softmax_rows(y.view(65536, 4096), x.view(65536, 4096), log=lg)
+            fn = lambda: L.softmax_rows_backward(gxo.view(65536, 4096), gg.view(65536, 4096),  # noqa: E731
+                                                 y.view(65536, 4096), log=lg)
+        elif w == "rowsbwd":
+            sr = torch.zeros(65536, device="cuda")
+            L.normalize_rows(y.view(65536, 4096), x.view(65536, 4096).abs(), index="dense", sum_out=sr)
+            fn = lambda: L.normalize_rows_backward(gxo.view(65536, 4096), gg.view(65536, 4096),  # noqa: E731
+                                                   y.view(65536, 4096), sr, index="dense")
+        else:
+            idx = "literal" if w.endswith("l") else "dense"
+            sv = torch.zeros(1, device="cuda")
+            y.copy_(x.abs())
+            L.normalize(y, y, index=idx, sum_out=sv)
+            fn = lambda: L.normalize_backward(gxo, gg, y, sv, index=idx)  # noqa: E731
     else:
         continue
     med, mn = timed(fn)
