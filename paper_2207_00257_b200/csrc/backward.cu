@@ -30,6 +30,18 @@ constexpr int BW_THREADS = 256;
 #define NORM_BW_ROW_CTAS 8
 #endif
 constexpr int BW_ROW_CTAS_PER_SM = NORM_BW_ROW_CTAS;
+// Register-resident rows kernel where it applies (rows of <= 4096 floats, 32-byte
+// aligned), 3 CTAs per SM; NORM_BW_REG=0 / NORM_BW_REG_MINB: probe builds only.
+// Same box, 65536 x 4096, us per call (profiles/round2/backward/ab_bwreg*.txt):
+// softmax / log-softmax / rows-normalize backward 499 / 468 / 505 at 3 CTAs/SM vs
+// 503 / 478 / ~548 for the two-sweep kernel (4 CTAs/SM: 513 / 511 / 486; 5: 502 /
+// 506 / 508-551).
+#ifndef NORM_BW_REG
+#define NORM_BW_REG 1
+#endif
+#ifndef NORM_BW_REG_MINB
+#define NORM_BW_REG_MINB 3
+#endif
 
 __device__ __forceinline__ bool bw_cov(int64_t i, int64_t L, int64_t G) {
   return L >= 0 ? i < L : (i % 32) < G;
@@ -138,6 +150,64 @@ __global__ void __launch_bounds__(BW_THREADS, NORM_BW_MINB)
     } else {
       for (int64_t j = threadIdx.x; j < cols; j += BW_THREADS)
         xr[j] = bw_out<KIND>(gr[j], yr[j], bw_cov(j, L, G), D, dv);
+    }
+  }
+}
+
+// Register-resident rows (32-byte aligned, cols % 8 == 0, cols <= 2048 MAXV): the
+// row's g and y are loaded once with 256-bit loads and kept in registers across
+// the block reduction, so the elementwise pass re-reads nothing.
+template <int KIND, int MAXV>
+__global__ void __launch_bounds__(BW_THREADS, NORM_BW_REG_MINB)
+    rows_bwd_reg_kernel(float* gx, const float* g, const float* y, const float* s_rows, int64_t rows,
+                        int64_t cols, int64_t ld, int64_t L, int64_t G) {
+  __shared__ double red[2][BW_THREADS / 32];
+  const int nv = (int)(cols >> 3);
+  int par = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, par ^= 1) {
+    const float* gr = g + r * ld;
+    const float* yr = y + r * ld;
+    f8 a[MAXV], b[MAXV];
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int idx = k * BW_THREADS + threadIdx.x;
+      if (idx < nv) {
+        a[k] = ld8(gr + (int64_t)idx * 8);
+        b[k] = ld8(yr + (int64_t)idx * 8);
+      }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int idx = k * BW_THREADS + threadIdx.x;
+      if (idx < nv) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t += bw_term<KIND>(a[k].v[j], b[k].v[j], bw_cov((int64_t)idx * 8 + j, L, G));
+        acc += t;
+      }
+    }
+    const double Dsum = block_sum_1b(acc, red[par]);
+    float s = 1.0f, D;
+    if (KIND == BW_NORMALIZE) {
+      s = s_rows[r];
+      D = (float)(Dsum / (double)s);
+    } else {
+      D = (float)Dsum;
+    }
+    const Divisor dv = make_divisor(s);
+    float* xr = gx + r * ld;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int idx = k * BW_THREADS + threadIdx.x;
+      if (idx < nv) {
+        const int64_t e = (int64_t)idx * 8;
+        const float4 lo = bw_out4<KIND>(make_float4(a[k].v[0], a[k].v[1], a[k].v[2], a[k].v[3]),
+                                        make_float4(b[k].v[0], b[k].v[1], b[k].v[2], b[k].v[3]), e, L, G, D, dv);
+        const float4 hi = bw_out4<KIND>(make_float4(a[k].v[4], a[k].v[5], a[k].v[6], a[k].v[7]),
+                                        make_float4(b[k].v[4], b[k].v[5], b[k].v[6], b[k].v[7]), e + 4, L, G, D, dv);
+        st8_stream(xr + e, f8{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}});
+      }
     }
   }
 }
@@ -258,6 +328,24 @@ cudaError_t launch_rows_backward(float* gx, const float* g, const float* y, cons
   const bool vec = aligned16(gx) && aligned16(g) && aligned16(y) && (cols % 4) == 0 && (ld % 4) == 0;
   int64_t gd = (int64_t)d.sms * BW_ROW_CTAS_PER_SM;
   if (rows < gd) gd = rows;
+#if NORM_BW_REG
+  const bool reg = ((reinterpret_cast<uintptr_t>(gx) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(y)) & 31u) == 0 && (cols % 8) == 0 && (ld % 8) == 0 &&
+                   cols <= BW_THREADS * 8 * 2;
+  if (reg) {
+    int64_t gr = (int64_t)d.sms * NORM_BW_REG_MINB;
+    if (rows < gr) gr = rows;
+    const bool two = cols > BW_THREADS * 8;
+#define NORM_BWR(K)                                                                                 \
+  (two ? rows_bwd_reg_kernel<K, 2><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G) \
+       : rows_bwd_reg_kernel<K, 1><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G))
+    if (kind == BW_NORMALIZE) NORM_BWR(BW_NORMALIZE);
+    else if (kind == BW_SOFTMAX) NORM_BWR(BW_SOFTMAX);
+    else NORM_BWR(BW_LOG_SOFTMAX);
+#undef NORM_BWR
+    return cudaGetLastError();
+  }
+#endif
 #define NORM_BW(K, V) \
   rows_bwd_kernel<K, V><<<(int)gd, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G)
   if (kind == BW_NORMALIZE) {
