@@ -17,8 +17,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
-#include "device_common.cuh"
-#include "norm_internal.h"
+#include "stream_common.cuh"
 
 namespace lnorm {
 
@@ -243,6 +242,7 @@ __global__ void __launch_bounds__(BW_THREADS, 4)
   } else {
     for (int64_t j = tid; j < len; j += nth) acc += bw_term<BW_NORMALIZE>(g[j], y[j], bw_cov(j, L, G));
   }
+  pdl_launch_dependents();  // the tile kernel may start loading g (this kernel never writes it)
   const double b = block_sum(acc, red);
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = b;
@@ -297,6 +297,43 @@ __global__ void __launch_bounds__(BW_THREADS, 4)
   }
 }
 
+// Elementwise pass as the forward's scale_tile_kernel: a non-persistent grid of
+// one 2048-float tile per CTA (one 256-bit load per thread, issued before
+// griddepcontrol.wait: the dot kernel does not write g), the last CTA takes the
+// unaligned head and the ragged tail.  Prefix coverage [0, L); g and gx
+// co-aligned mod 32 bytes.
+constexpr int BWT_THREADS = 256;
+constexpr int64_t BWT_F = (int64_t)BWT_THREADS * 8;
+
+template <bool ALIAS>
+__global__ void __launch_bounds__(BWT_THREADS)
+    vec_bwd_tile_kernel(float* gx, const float* g, int64_t n, int64_t L, int64_t head, int64_t ntiles,
+                        const float* s, const double* D_in) {
+  const bool body = (int64_t)blockIdx.x < ntiles;
+  const int64_t off = head + (int64_t)blockIdx.x * BWT_F + (int64_t)threadIdx.x * 8;
+  f8 v;
+  if (body) v = ALIAS ? ld8(g + off) : ld8_stream(g + off);
+  pdl_wait();
+  const Divisor dv = make_divisor(*s);
+  const float D = (float)__ldcg(D_in);
+  if (body) {
+    f8 o;
+    if (off + 8 <= L) {
+      o = div8(v, dv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o.v[j] -= D;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o.v[j] = bw_out<BW_NORMALIZE>(v.v[j], 0.f, off + j < L, D, dv);
+    }
+    st8_stream(gx + off, o);
+    return;
+  }
+  for (int64_t i = threadIdx.x; i < head; i += BWT_THREADS) gx[i] = bw_out<BW_NORMALIZE>(g[i], 0.f, i < L, D, dv);
+  for (int64_t i = head + ntiles * BWT_F + threadIdx.x; i < n; i += BWT_THREADS)
+    gx[i] = bw_out<BW_NORMALIZE>(g[i], 0.f, i < L, D, dv);
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 cudaError_t launch_normalize_backward(float* gx, const float* g, const float* y, const float* s,
@@ -313,6 +350,19 @@ cudaError_t launch_normalize_backward(float* gx, const float* g, const float* y,
     vec_bwd_dot_kernel<false><<<(int)gd, BW_THREADS, 0, st>>>(g, y, cov.n, L, cov.G, s, ws.partials, ws.ticket, D);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  // tile kernel when g and gx are co-aligned mod 32 B (the common case)
+  const uintptr_t pg = reinterpret_cast<uintptr_t>(g), px = reinterpret_cast<uintptr_t>(gx);
+  if (vec && ((pg ^ px) & 31u) == 0) {
+    int64_t head = (int64_t)(((32u - (pg & 31u)) & 31u) / 4);
+    if (head > cov.n) head = cov.n;
+    const int64_t ntiles = (cov.n - head) / BWT_F;
+    if (ntiles + 1 <= 2147483647LL) {
+      return gx == g ? launch_maybe_pdl(vec_bwd_tile_kernel<true>, (int)(ntiles + 1), BWT_THREADS, true, st, gx,
+                                        g, cov.n, L, head, ntiles, s, (const double*)D)
+                     : launch_maybe_pdl(vec_bwd_tile_kernel<false>, (int)(ntiles + 1), BWT_THREADS, true, st, gx,
+                                        g, cov.n, L, head, ntiles, s, (const double*)D);
+    }
+  }
   const int64_t ga = (int64_t)d.sms * 8;
   if (vec)
     vec_bwd_apply_kernel<true><<<(int)ga, BW_THREADS, 0, st>>>(gx, g, cov.n, L, cov.G, s, D);
