@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include "stream_common.cuh"
 
 namespace lnorm {
@@ -30,7 +33,10 @@ constexpr int BW_THREADS = 256;
 #endif
 constexpr int BW_ROW_CTAS_PER_SM = NORM_BW_ROW_CTAS;
 // Register-resident rows kernel where it applies (rows of <= 4096 floats, 32-byte
-// aligned), 3 CTAs per SM; NORM_BW_REG=0 / NORM_BW_REG_MINB: probe builds only.
+// aligned), 3 CTAs per SM, rows from a queue (NORM_ROWS_QUEUE=0: grid-strided;
+// same box: softmax / log-softmax / rows-normalize backward 457 / 457 / 492 us vs
+// 495 / 496 / 509, profiles/round2/backward/ab_row_queue.txt);
+// NORM_BW_REG=0 / NORM_BW_REG_MINB: probe builds only.
 // Same box, 65536 x 4096, us per call (profiles/round2/backward/ab_bwreg*.txt):
 // softmax / log-softmax / rows-normalize backward 499 / 468 / 505 at 3 CTAs/SM vs
 // 503 / 478 / ~548 for the two-sweep kernel (4 CTAs/SM: 513 / 511 / 486; 5: 502 /
@@ -159,11 +165,21 @@ __global__ void __launch_bounds__(BW_THREADS, NORM_BW_MINB)
 template <int KIND, int MAXV>
 __global__ void __launch_bounds__(BW_THREADS, NORM_BW_REG_MINB)
     rows_bwd_reg_kernel(float* gx, const float* g, const float* y, const float* s_rows, int64_t rows,
-                        int64_t cols, int64_t ld, int64_t L, int64_t G) {
+                        int64_t cols, int64_t ld, int64_t L, int64_t G, unsigned* ctr) {
+  // ctr != NULL: rows from a queue (as the forward rows kernels): thread 0 claims
+  // the next row before the current row's barrier and publishes it across it,
+  // so CTAs on faster SMs take more rows; the last CTA to run dry resets it.
   __shared__ double red[2][BW_THREADS / 32];
+  __shared__ int64_t claim[2];
   const int nv = (int)(cols >> 3);
   int par = 0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, par ^= 1) {
+  int64_t r = blockIdx.x;
+  if (ctr) {
+    if (threadIdx.x == 0) claim[0] = (int64_t)atomicAdd(ctr, 1u);
+    __syncthreads();
+    r = claim[0];
+  }
+  while (r < rows) {
     const float* gr = g + r * ld;
     const float* yr = y + r * ld;
     f8 a[MAXV], b[MAXV];
@@ -175,6 +191,7 @@ __global__ void __launch_bounds__(BW_THREADS, NORM_BW_REG_MINB)
         b[k] = ld8(yr + (int64_t)idx * 8);
       }
     }
+    if (ctr && threadIdx.x == 0) claim[par ^ 1] = r < rows ? (int64_t)atomicAdd(ctr, 1u) : rows;
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < MAXV; ++k) {
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(BW_THREADS, NORM_BW_REG_MINB)
         acc += t;
       }
     }
-    const double Dsum = block_sum_1b(acc, red[par]);
+    const double Dsum = block_sum_1b(acc, red[par]);  // its barrier also publishes claim[par ^ 1]
     float s = 1.0f, D;
     if (KIND == BW_NORMALIZE) {
       s = s_rows[r];
@@ -207,6 +224,16 @@ __global__ void __launch_bounds__(BW_THREADS, NORM_BW_REG_MINB)
                                         make_float4(b[k].v[4], b[k].v[5], b[k].v[6], b[k].v[7]), e + 4, L, G, D, dv);
         st8_stream(xr + e, f8{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}});
       }
+    }
+    r = ctr ? claim[par ^ 1] : r + gridDim.x;
+    par ^= 1;
+  }
+  if (ctr && threadIdx.x == 0) {
+    __threadfence();  // this CTA's claims on ctr[0] precede its count on ctr[1]
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+      __threadfence();  // every other CTA's claims are visible before the reset
+      ctr[0] = 0u;
+      ctr[1] = 0u;
     }
   }
 }
@@ -373,7 +400,12 @@ cudaError_t launch_normalize_backward(float* gx, const float* g, const float* y,
 
 cudaError_t launch_rows_backward(float* gx, const float* g, const float* y, const float* s_rows,
                                  int64_t rows, int64_t cols, int64_t ld, int kind, const Coverage& rc,
-                                 const DeviceInfo& d, cudaStream_t st) {
+                                 const DeviceInfo& d, cudaStream_t st, unsigned* row_ctr) {
+  static const bool queue = [] {  // NORM_ROWS_QUEUE=0: grid-strided rows (A/B knob)
+    const char* e = getenv("NORM_ROWS_QUEUE");
+    return !(e && !strcmp(e, "0"));
+  }();
+  unsigned* rq = queue && rows < (1ll << 31) ? row_ctr : nullptr;  // 32-bit claim counter
   const int64_t L = kind != BW_NORMALIZE ? cols : (rc.kind == COV_PREFIX ? rc.L : -1);
   const bool vec = aligned16(gx) && aligned16(g) && aligned16(y) && (cols % 4) == 0 && (ld % 4) == 0;
   int64_t gd = (int64_t)d.sms * BW_ROW_CTAS_PER_SM;
@@ -387,8 +419,8 @@ cudaError_t launch_rows_backward(float* gx, const float* g, const float* y, cons
     if (rows < gr) gr = rows;
     const bool two = cols > BW_THREADS * 8;
 #define NORM_BWR(K)                                                                                 \
-  (two ? rows_bwd_reg_kernel<K, 2><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G) \
-       : rows_bwd_reg_kernel<K, 1><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G))
+  (two ? rows_bwd_reg_kernel<K, 2><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G, rq) \
+       : rows_bwd_reg_kernel<K, 1><<<(int)gr, BW_THREADS, 0, st>>>(gx, g, y, s_rows, rows, cols, ld, L, rc.G, rq))
     if (kind == BW_NORMALIZE) NORM_BWR(BW_NORMALIZE);
     else if (kind == BW_SOFTMAX) NORM_BWR(BW_SOFTMAX);
     else NORM_BWR(BW_LOG_SOFTMAX);

@@ -816,9 +816,11 @@ static norm_status_t rows_backward(float* gx, const float* g, const float* y, co
   if ((st = check_device(&d)) != NORM_OK) return st;
   if ((st = check_bwd_ptrs(gx, g, y, kind == BW_NORMALIZE ? s : nullptr, d, o)) != NORM_OK) return st;
   const Coverage rc = coverage_of(cols, o->index);
+  Workspace ws;
+  if ((st = get_workspace(o, d.device, static_cast<cudaStream_t>(o->stream), &ws)) != NORM_OK) return st;
   NvtxRange r("norm_rows_backward");
   const cudaError_t e = launch_rows_backward(gx, g, y, s, rows, cols, ld, kind, rc, d,
-                                             static_cast<cudaStream_t>(o->stream));
+                                             static_cast<cudaStream_t>(o->stream), ws.row_ctr);
   return e == cudaSuccess ? NORM_OK : cuda_fail(e, "rows backward launch");
 }
 

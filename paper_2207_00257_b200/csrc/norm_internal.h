@@ -168,7 +168,7 @@ cudaError_t launch_normalize_backward(float* gx, const float* g, const float* y,
                                       cudaStream_t st);
 cudaError_t launch_rows_backward(float* gx, const float* g, const float* y, const float* s_rows,
                                  int64_t rows, int64_t cols, int64_t ld, int kind, const Coverage& rc,
-                                 const DeviceInfo& d, cudaStream_t st);
+                                 const DeviceInfo& d, cudaStream_t st, unsigned* row_ctr);
 
 // NEXT-4 backprop layerforward (backprop.cu)
 cudaError_t launch_bpnn(const float* input, float* hidden, float* output, int64_t in, int64_t hid,
